@@ -1,0 +1,87 @@
+"""Builds the B200 executor library `_lib/libtcg.so` in-tree.
+
+Host C++ (planner, runtime, C-ABI) is compiled by g++; the CUDA executors by
+nvcc for sm_100a only (`-gencode arch=compute_100a,code=sm_100a`), with
+`-fmad=false` so fp64 per-point arithmetic is never contracted into FMAs
+(bit parity with the reference's FMA-free host build).
+Incremental: an object is rebuilt when any source or header is newer.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+LIB_DIR = PKG / "_lib"
+OBJ_DIR = LIB_DIR / "obj"
+LIB = LIB_DIR / "libtcg.so"
+REPO = PKG.parent
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CXXFLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra", "-Wno-unused-parameter",
+            f"-I{REPO / 'include'}", "-I/usr/local/cuda/include"]
+NVCCFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler", "-fPIC",
+                    "--expt-relaxed-constexpr", "-Xptxas", "-v", f"-I{REPO / 'include'}"]
+
+HOST_SRCS = ["host/tcg_plan.cpp", "host/tcg_gpuplan.cpp", "host/tcg_runtime.cpp", "tcg_capi.cpp"]
+CUDA_SRCS = ["cuda/tcg_exec.cu"]
+
+
+def _headers() -> list[Path]:
+    hs = [p for p in CSRC.rglob("*.h*")]
+    hs += list((REPO / "include").glob("*.h"))
+    return hs
+
+
+def _stale(obj: Path, src: Path, headers: list[Path]) -> bool:
+    if not obj.exists():
+        return True
+    t = obj.stat().st_mtime
+    return src.stat().st_mtime > t or any(h.stat().st_mtime > t for h in headers)
+
+
+def _compile(cmd: list[str], log: Path) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    log.write_text(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"compile failed: {' '.join(cmd)}")
+
+
+def build(verbose: bool = False) -> Path:
+    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+    headers = _headers()
+    jobs = []
+    objs = []
+    for s in HOST_SRCS:
+        src = CSRC / s
+        obj = OBJ_DIR / (s.replace("/", "_") + ".o")
+        objs.append(obj)
+        if _stale(obj, src, headers):
+            jobs.append(([CXX, *CXXFLAGS, "-c", str(src), "-o", str(obj)], obj.with_suffix(".log")))
+    for s in CUDA_SRCS:
+        src = CSRC / s
+        obj = OBJ_DIR / (s.replace("/", "_") + ".o")
+        objs.append(obj)
+        if _stale(obj, src, headers):
+            jobs.append(([NVCC, *NVCCFLAGS, "-c", str(src), "-o", str(obj)], obj.with_suffix(".log")))
+    if jobs:
+        with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
+            for f in [ex.submit(_compile, c, l) for c, l in jobs]:
+                f.result()
+    if jobs or not LIB.exists():
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcuda"]
+        _compile(cmd, LIB_DIR / "link.log")
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose=True)

@@ -1,0 +1,545 @@
+// CUDA executors for sm_100a (B200) -- the replacement of the reference's
+// CPU execute_untiled / execute_plan (proj/core/src/executor.cpp:124-277).
+//
+//   k_untiled<DIM>   one launch per loop over its recorded range, in place in
+//                    HBM (the "untiled" baseline, executor.cpp:252-277). Each
+//                    thread runs the loop's registered body at one point;
+//                    coalesced along x (dim 0 is fastest in memory).
+//   k_tiled<DIM>     the windowed tiled executor: one CTA per "rank" of an
+//                    overlapped CTA decomposition; each CTA executes its own
+//                    reference-style skewed rank plan on
+//                    shared-memory windows that slide along the slowest
+//                    dimension, so intermediate values of the chain never
+//                    leave the SM.
+//   k_fold           deterministic fixed-order fold of per-block reduction
+//                    partials (the reference folds worker partials in worker
+//                    order, executor.cpp:175-176).
+// All arithmetic is fp64 and compiled with -fmad=false so every per-point
+// expression rounds exactly like the reference's (FMA-free) host build.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "../host/tcg_exec.hpp"
+#include "../kernels/tc_bodies.h"
+
+namespace tcg {
+
+namespace {
+
+#define TCG_CK(x)                                                                         \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kTiledThreads = 512;
+constexpr int kMaxParams = 16;
+
+__host__ __device__ __forceinline__ double red_identity(int op) {
+  return op == 0 ? 0.0 : (op == 1 ? HUGE_VAL : -HUGE_VAL);
+}
+__device__ __forceinline__ double red_combine(int op, double a, double b) {
+  return op == 0 ? a + b : (op == 1 ? (a < b ? a : b) : (a > b ? a : b));
+}
+
+// Block-wide reduction, deterministic for a fixed block shape: xor-shuffle
+// tree inside each warp, then warp results in warp order. Result on thread 0.
+__device__ double block_reduce(double v, int op) {
+  __shared__ double ws[32];
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nthr = blockDim.x * blockDim.y * blockDim.z;
+  for (int o = 16; o > 0; o >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((tid & 31) == 0) ws[tid >> 5] = v;
+  __syncthreads();
+  if (tid < 32) {
+    const int nw = (nthr + 31) >> 5;
+    v = tid < nw ? ws[tid] : red_identity(op);
+    for (int o = 16; o > 0; o >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(1024) k_fold(const double* __restrict__ p, int64_t n, int op, double* out) {
+  const int64_t chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t a = static_cast<int64_t>(threadIdx.x) * chunk;
+  const int64_t b = a + chunk < n ? a + chunk : n;
+  double v = red_identity(op);
+  for (int64_t i = a; i < b; ++i) v = red_combine(op, v, p[i]);
+  v = block_reduce(v, op);
+  if (threadIdx.x == 0) *out = v;
+}
+
+// ---------------------------------------------------------------------------
+// Untiled per-loop executor.
+
+struct UArg {
+  double* base;
+  int64_t x0, y0, z0, py, pz;
+  int32_t mode, stencil;
+};
+
+struct ULaunch {
+  int32_t body, nargs, red_op, has_red;
+  int64_t lo[3], n[3];
+  UArg a[kMaxArgs];
+  double prm[kMaxParams];
+  DevStencils st;
+  double* partials;
+};
+
+struct GAcc {
+  const ULaunch& L;
+  int64_t px, py, pz;
+  double acc;
+  __device__ __forceinline__ double* at(int a, int dx, int dy, int dz) const {
+    const UArg& g = L.a[a];
+    return g.base + ((pz + dz - g.z0) * g.pz + (py + dy - g.y0) * g.py + (px + dx - g.x0));
+  }
+  __device__ __forceinline__ int64_t x() const { return px; }
+  __device__ __forceinline__ int64_t y() const { return py; }
+  __device__ __forceinline__ int64_t z() const { return pz; }
+  __device__ __forceinline__ double read(int a, int dx, int dy, int dz) const { return *at(a, dx, dy, dz); }
+  __device__ __forceinline__ void write(int a, double v) const { *at(a, 0, 0, 0) = v; }
+  __device__ __forceinline__ void increment(int a, double v) const {
+    double* p = at(a, 0, 0, 0);
+    *p = *p + v;
+  }
+  __device__ __forceinline__ void contribute(double v) { acc = red_combine(L.red_op, acc, v); }
+  __device__ __forceinline__ int nargs() const { return L.nargs; }
+  __device__ __forceinline__ int mode(int a) const { return L.a[a].mode; }
+  __device__ __forceinline__ int npts(int a) const { return L.st.npts[L.a[a].stencil]; }
+  __device__ __forceinline__ int pt(int a, int j, int d) const {
+    return L.st.pts[3 * (L.st.start[L.a[a].stencil] + j) + d];
+  }
+  __device__ __forceinline__ bool reduces() const { return L.has_red != 0; }
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch L) {
+  int64_t x, y = 0, z = 0;
+  bool active;
+  if (DIM == 1) {
+    x = L.lo[0] + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    active = x < L.lo[0] + L.n[0];
+  } else {
+    x = L.lo[0] + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    y = L.lo[1] + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+    if (DIM == 3) z = L.lo[2] + blockIdx.z;
+    active = x < L.lo[0] + L.n[0] && y < L.lo[1] + L.n[1];
+  }
+  GAcc acc{L, x, y, z, red_identity(L.red_op)};
+  if (active) tcb::run_body(L.body, acc, L.prm);
+  if (L.has_red) {
+    const double v = block_reduce(acc.acc, L.red_op);
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      L.partials[blockIdx.x + static_cast<int64_t>(gridDim.x) * (blockIdx.y + static_cast<int64_t>(gridDim.y) * blockIdx.z)] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Windowed tiled executor.
+#include "tcg_tiled.cuh"
+
+
+template <int DIM>
+void set_tiled_smem(int64_t bytes) {
+  TCG_CK(cudaFuncSetAttribute(tiled::k_tiled<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Host side.
+
+struct DeviceExec::Buf {
+  Range alloc;
+  int64_t x0 = 0, nxp = 0, py = 0, pz = 0, ny = 1, nz = 1;
+  double* mem[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+  int cur = 0;
+};
+
+struct DeviceExec::PlanBufs {
+  void* mem = nullptr;
+  DevCta* ctas = nullptr;
+  int32_t* boxes = nullptr;
+  int32_t* win = nullptr;
+  int32_t* wboxes = nullptr;
+};
+
+DeviceExec::DeviceExec() {
+  int ndev = 0;
+  TCG_CK(cudaGetDeviceCount(&ndev));
+  if (ndev <= 0) throw CudaError("no CUDA device visible: the B200 executor has no CPU fallback");
+  TCG_CK(cudaGetDevice(&info_.device));
+  cudaDeviceProp prop;
+  TCG_CK(cudaGetDeviceProperties(&prop, info_.device));
+  info_.num_sms = prop.multiProcessorCount;
+  info_.smem_optin = static_cast<int64_t>(prop.sharedMemPerBlockOptin);
+  info_.l2_bytes = prop.l2CacheSize;
+  info_.name = prop.name;
+  if (prop.major < 10) throw CudaError("executor is built for sm_100a (B200); found " + info_.name);
+  cudaStream_t st;
+  TCG_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  stream_ = st;
+  TCG_CK(cudaMalloc(&red_dev_, sizeof(double) * 64));
+}
+
+DeviceExec::~DeviceExec() {
+  for (Buf* b : fields_) {
+    if (b->mem[0]) cudaFree(b->mem[0]);
+    if (b->mem[1]) cudaFree(b->mem[1]);
+    delete b;
+  }
+  for (auto& pb : plan_cache_) {
+    cudaFree(pb.second->mem);
+    delete pb.second;
+  }
+  if (scratch_) cudaFree(scratch_);
+  if (partials_) cudaFree(partials_);
+  if (red_dev_) cudaFree(red_dev_);
+  if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+}
+
+int DeviceExec::add_field(const Range& alloc) {
+  auto* b = new Buf;
+  b->alloc = alloc;
+  const int dim = alloc.dim();
+  const int64_t ax0 = alloc.start(0), ax1 = alloc.end(0);
+  // x origin: a multiple of 16 at least 16 elements before the allocation.
+  auto fl16 = [](int64_t v) { return v >= 0 ? v / 16 * 16 : -((-v + 15) / 16) * 16; };
+  b->x0 = fl16(ax0) - 16;
+  b->py = ((ax1 + 16 - b->x0) + 15) / 16 * 16;
+  b->ny = dim >= 2 ? alloc.extent(1) : 1;
+  b->nz = dim >= 3 ? alloc.extent(2) : 1;
+  b->pz = b->py * b->ny;
+  b->bytes = static_cast<size_t>(b->pz * b->nz) * sizeof(double);
+  TCG_CK(cudaMalloc(&b->mem[0], b->bytes));
+  TCG_CK(cudaMemsetAsync(b->mem[0], 0, b->bytes, static_cast<cudaStream_t>(stream_)));
+  fields_.push_back(b);
+  return static_cast<int>(fields_.size()) - 1;
+}
+
+int64_t DeviceExec::field_bytes(int f) const { return static_cast<int64_t>(fields_.at(static_cast<size_t>(f))->bytes); }
+
+DevView DeviceExec::view(int f, bool alt) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  const int which = alt ? 1 - b->cur : b->cur;
+  if (!b->mem[which]) {
+    TCG_CK(cudaMalloc(&b->mem[which], b->bytes));
+    TCG_CK(cudaMemsetAsync(b->mem[which], 0, b->bytes, static_cast<cudaStream_t>(stream_)));
+  }
+  DevView v{};
+  const int dim = b->alloc.dim();
+  v.base = b->mem[which];
+  v.x0 = b->x0;
+  v.y0 = dim >= 2 ? b->alloc.start(1) : 0;
+  v.z0 = dim >= 3 ? b->alloc.start(2) : 0;
+  v.py = b->py;
+  v.pz = dim >= 3 ? b->pz : 0;
+  if (dim < 2) v.py = 0;
+  for (int d = 0; d < 3; ++d) {
+    v.alo[d] = d < dim ? b->alloc.start(d) : 0;
+    v.ahi[d] = d < dim ? b->alloc.end(d) : 1;
+  }
+  return v;
+}
+
+void DeviceExec::swap(int f) { fields_.at(static_cast<size_t>(f))->cur ^= 1; }
+
+namespace {
+double* point_addr(const DevView& v, const Range& alloc, const Point& p) {
+  if (!alloc.contains(p)) throw AccessError("point outside allocated extent " + alloc.to_string());
+  return v.base + ((p[2] - v.z0) * v.pz + (p[1] - v.y0) * v.py + (p[0] - v.x0));
+}
+}  // namespace
+
+double DeviceExec::get_point(int f, const Point& p) {
+  const DevView v = view(f, false);
+  double out = 0;
+  TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+  TCG_CK(cudaMemcpy(&out, point_addr(v, fields_.at(static_cast<size_t>(f))->alloc, p), 8, cudaMemcpyDeviceToHost));
+  return out;
+}
+
+void DeviceExec::put_point(int f, const Point& p, double val) {
+  const DevView v = view(f, false);
+  TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+  TCG_CK(cudaMemcpy(point_addr(v, fields_.at(static_cast<size_t>(f))->alloc, p), &val, 8, cudaMemcpyHostToDevice));
+}
+
+namespace {
+void copy2d(DeviceExec& ex, int f, double* dev, int64_t x0, int64_t py, const Range& alloc, double* host, bool up,
+            bool async, cudaStream_t st) {
+  const int64_t nx = alloc.extent(0);
+  const int64_t rows = alloc.volume() / std::max<int64_t>(1, nx);
+  double* d = dev + (alloc.start(0) - x0);
+  const size_t w = static_cast<size_t>(nx) * sizeof(double);
+  (void)ex;
+  (void)f;
+  if (up)
+    TCG_CK(cudaMemcpy2DAsync(d, static_cast<size_t>(py) * sizeof(double), host, w, w, static_cast<size_t>(rows),
+                             cudaMemcpyHostToDevice, st));
+  else
+    TCG_CK(cudaMemcpy2DAsync(host, w, d, static_cast<size_t>(py) * sizeof(double), w, static_cast<size_t>(rows),
+                             cudaMemcpyDeviceToHost, st));
+  if (!async) TCG_CK(cudaStreamSynchronize(st));
+}
+}  // namespace
+
+void DeviceExec::upload(int f, const double* host) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  copy2d(*this, f, b->mem[b->cur], b->x0, b->alloc.dim() >= 2 ? b->py : b->py, b->alloc, const_cast<double*>(host),
+         true, false, static_cast<cudaStream_t>(stream_));
+}
+void DeviceExec::download(int f, double* host) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  copy2d(*this, f, b->mem[b->cur], b->x0, b->py, b->alloc, host, false, false, static_cast<cudaStream_t>(stream_));
+}
+void DeviceExec::upload_async(int f, const double* host) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  copy2d(*this, f, b->mem[b->cur], b->x0, b->py, b->alloc, const_cast<double*>(host), true, true,
+         static_cast<cudaStream_t>(stream_));
+}
+void DeviceExec::download_async(int f, double* host) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  copy2d(*this, f, b->mem[b->cur], b->x0, b->py, b->alloc, host, false, true, static_cast<cudaStream_t>(stream_));
+}
+
+void DeviceExec::synchronize() { TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_))); }
+
+void* DeviceExec::ensure_scratch(size_t bytes) {
+  if (bytes > scratch_bytes_) {
+    if (scratch_) {
+      TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+      TCG_CK(cudaFree(scratch_));
+    }
+    scratch_bytes_ = std::max(bytes, scratch_bytes_ * 2);
+    TCG_CK(cudaMalloc(&scratch_, scratch_bytes_));
+  }
+  return scratch_;
+}
+
+double* DeviceExec::ensure_partials(size_t n) {
+  if (n > partials_n_) {
+    if (partials_) {
+      TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+      TCG_CK(cudaFree(partials_));
+    }
+    partials_n_ = std::max(n, partials_n_ * 2);
+    TCG_CK(cudaMalloc(&partials_, partials_n_ * sizeof(double)));
+  }
+  return partials_;
+}
+
+int64_t DeviceExec::window_budget_doubles(int nloops, int nred) const {
+  const int64_t fixed = static_cast<int64_t>(sizeof(tiled::Shared)) + 512 + 256 + static_cast<int64_t>(nloops) * kMaxArgs * 16;
+  const int64_t bytes = info_.smem_optin - fixed - static_cast<int64_t>(nloops) * static_cast<int64_t>(sizeof(DevLoop)) -
+                        static_cast<int64_t>(nred) * kTiledThreads * 8;
+  return std::max<int64_t>(0, bytes / 8);
+}
+
+namespace {
+// Uploads the chain tables into scratch; returns device pointers.
+struct ChainDev {
+  DevLoop* loops;
+  double* params;
+  DevStencils st;
+};
+
+template <class T>
+size_t align_up(size_t v) {
+  return (v + 255) / 256 * 256 + 0 * sizeof(T);
+}
+
+ChainDev upload_chain(const DevChain& ch, void* scratch, cudaStream_t st) {
+  const size_t nl = ch.loops.size() * sizeof(DevLoop);
+  const size_t np = std::max<size_t>(1, ch.params.size()) * sizeof(double);
+  const size_t ns = std::max<size_t>(1, ch.st_start.size()) * 4;
+  const size_t nq = std::max<size_t>(1, ch.st_pts.size()) * 4;
+  char* base = static_cast<char*>(scratch);
+  size_t off = 0;
+  ChainDev cd;
+  cd.loops = reinterpret_cast<DevLoop*>(base + off);
+  if (nl) TCG_CK(cudaMemcpyAsync(base + off, ch.loops.data(), nl, cudaMemcpyHostToDevice, st));
+  off += align_up<char>(nl);
+  cd.params = reinterpret_cast<double*>(base + off);
+  if (!ch.params.empty())
+    TCG_CK(cudaMemcpyAsync(base + off, ch.params.data(), ch.params.size() * 8, cudaMemcpyHostToDevice, st));
+  off += align_up<char>(np);
+  int32_t* s0 = reinterpret_cast<int32_t*>(base + off);
+  if (!ch.st_start.empty()) TCG_CK(cudaMemcpyAsync(s0, ch.st_start.data(), ch.st_start.size() * 4, cudaMemcpyHostToDevice, st));
+  off += align_up<char>(ns);
+  int32_t* s1 = reinterpret_cast<int32_t*>(base + off);
+  if (!ch.st_npts.empty()) TCG_CK(cudaMemcpyAsync(s1, ch.st_npts.data(), ch.st_npts.size() * 4, cudaMemcpyHostToDevice, st));
+  off += align_up<char>(ns);
+  int32_t* s2 = reinterpret_cast<int32_t*>(base + off);
+  if (!ch.st_pts.empty()) TCG_CK(cudaMemcpyAsync(s2, ch.st_pts.data(), ch.st_pts.size() * 4, cudaMemcpyHostToDevice, st));
+  cd.st = DevStencils{s0, s1, s2};
+  return cd;
+}
+
+size_t chain_bytes(const DevChain& ch) {
+  return align_up<char>(ch.loops.size() * sizeof(DevLoop)) + align_up<char>(std::max<size_t>(1, ch.params.size()) * 8) +
+         2 * align_up<char>(std::max<size_t>(1, ch.st_start.size()) * 4) +
+         align_up<char>(std::max<size_t>(1, ch.st_pts.size()) * 4) + 256;
+}
+}  // namespace
+
+void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  void* scratch = ensure_scratch(chain_bytes(ch));
+  const ChainDev cd = upload_chain(ch, scratch, st);
+  for (const DevLoop& lp : ch.loops) {
+    ULaunch L{};
+    L.body = lp.body;
+    L.nargs = lp.nargs;
+    L.red_op = lp.red >= 0 ? lp.red_op : 0;
+    L.has_red = lp.red >= 0;
+    int64_t n[3];
+    bool empty = false;
+    for (int d = 0; d < 3; ++d) {
+      L.lo[d] = lp.range[d][0];
+      n[d] = lp.range[d][1] - lp.range[d][0];
+      L.n[d] = n[d];
+      if (n[d] <= 0) empty = true;
+    }
+    if (lp.nparams > kMaxParams) throw InvalidArgument("untiled executor: more than 16 scalar params in one loop");
+    for (int i = 0; i < lp.nparams; ++i) L.prm[i] = ch.params[static_cast<size_t>(lp.param_off + i)];
+    for (int a = 0; a < lp.nargs; ++a) {
+      const DevView v = view(ch.dat_ids.empty() ? lp.args[a].dat : ch.dat_ids[static_cast<size_t>(lp.args[a].dat)], false);
+      L.a[a] = UArg{v.base, v.x0, v.y0, v.z0, v.py, v.pz, lp.args[a].mode, lp.args[a].stencil};
+    }
+    L.st = cd.st;
+    dim3 block, grid;
+    if (ch.dim == 1) {
+      block = dim3(256, 1, 1);
+      grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + 255) / 256)), 1, 1);
+    } else {
+      block = dim3(32, 8, 1);
+      grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + 31) / 32)),
+                  static_cast<unsigned>(std::max<int64_t>(1, (n[1] + 7) / 8)),
+                  static_cast<unsigned>(ch.dim == 3 ? std::max<int64_t>(1, n[2]) : 1));
+    }
+    const int64_t nblocks = static_cast<int64_t>(grid.x) * grid.y * grid.z;
+    if (L.has_red) L.partials = ensure_partials(static_cast<size_t>(nblocks));
+    if (empty) {
+      if (L.has_red) {
+        // Empty reducing loop: the result is the identity.
+        const double idv = red_identity(L.red_op);
+        TCG_CK(cudaMemcpyAsync(red_dev_ + lp.red, &idv, 8, cudaMemcpyHostToDevice, st));
+        TCG_CK(cudaStreamSynchronize(st));
+      }
+      continue;
+    }
+    if (ch.dim == 1)
+      k_untiled<1><<<grid, block, 0, st>>>(L);
+    else if (ch.dim == 2)
+      k_untiled<2><<<grid, block, 0, st>>>(L);
+    else
+      k_untiled<3><<<grid, block, 0, st>>>(L);
+    TCG_CK(cudaGetLastError());
+    ++launches_;
+    if (L.has_red) {
+      k_fold<<<1, 1024, 0, st>>>(L.partials, nblocks, L.red_op, red_dev_ + lp.red);
+      TCG_CK(cudaGetLastError());
+      ++launches_;
+    }
+  }
+  if (ch.nred > 0) {
+    TCG_CK(cudaMemcpyAsync(red_out, red_dev_, sizeof(double) * static_cast<size_t>(ch.nred), cudaMemcpyDeviceToHost, st));
+    TCG_CK(cudaStreamSynchronize(st));
+  }
+}
+
+DeviceExec::PlanBufs* DeviceExec::plan_bufs(const GpuTiledPlan& gp, uint64_t key) {
+  for (auto& pb : plan_cache_)
+    if (pb.first == key) return pb.second;
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  auto* pb = new PlanBufs;
+  const size_t a = align_up<char>(gp.ctas.size() * sizeof(DevCta));
+  const size_t b = align_up<char>(std::max<size_t>(1, gp.boxes.size()) * 4);
+  const size_t c = align_up<char>(std::max<size_t>(1, gp.win.size()) * 4);
+  const size_t d = align_up<char>(std::max<size_t>(1, gp.wboxes.size()) * 4);
+  TCG_CK(cudaMalloc(&pb->mem, a + b + c + d));
+  char* m = static_cast<char*>(pb->mem);
+  pb->ctas = reinterpret_cast<DevCta*>(m);
+  pb->boxes = reinterpret_cast<int32_t*>(m + a);
+  pb->win = reinterpret_cast<int32_t*>(m + a + b);
+  pb->wboxes = reinterpret_cast<int32_t*>(m + a + b + c);
+  TCG_CK(cudaMemcpyAsync(pb->ctas, gp.ctas.data(), gp.ctas.size() * sizeof(DevCta), cudaMemcpyHostToDevice, st));
+  if (!gp.boxes.empty()) TCG_CK(cudaMemcpyAsync(pb->boxes, gp.boxes.data(), gp.boxes.size() * 4, cudaMemcpyHostToDevice, st));
+  if (!gp.win.empty()) TCG_CK(cudaMemcpyAsync(pb->win, gp.win.data(), gp.win.size() * 4, cudaMemcpyHostToDevice, st));
+  if (!gp.wboxes.empty())
+    TCG_CK(cudaMemcpyAsync(pb->wboxes, gp.wboxes.data(), gp.wboxes.size() * 4, cudaMemcpyHostToDevice, st));
+  TCG_CK(cudaStreamSynchronize(st));
+  plan_cache_.emplace_back(key, pb);
+  if (plan_cache_.size() > 64) {
+    cudaFree(plan_cache_.front().second->mem);
+    delete plan_cache_.front().second;
+    plan_cache_.erase(plan_cache_.begin());
+  }
+  return pb;
+}
+
+void DeviceExec::run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t key, double* red_out) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  PlanBufs* pb = plan_bufs(gp, key);
+  void* scratch = ensure_scratch(chain_bytes(ch));
+  const ChainDev cd = upload_chain(ch, scratch, st);
+  DevTiledPlan P{};
+  P.dim = gp.dim;
+  P.nloops = gp.nloops;
+  P.ndat = gp.ndat;
+  P.nred = gp.nred;
+  P.nctas = static_cast<int32_t>(gp.ctas.size());
+  P.smem_doubles = static_cast<int32_t>((gp.smem_doubles + 1) / 2 * 2);
+  P.ctas = pb->ctas;
+  P.boxes = pb->boxes;
+  P.win = pb->win;
+  P.wboxes = pb->wboxes;
+  P.loops = cd.loops;
+  P.params = cd.params;
+  P.stencils = cd.st;
+  for (int k = 0; k < gp.ndat; ++k) {
+    P.dats[k] = gp.dats[static_cast<size_t>(k)];
+    const int f = gp.dat_ids[static_cast<size_t>(k)];
+    P.src[k] = view(f, false);
+    P.dst[k] = gp.dats[static_cast<size_t>(k)].pingpong ? view(f, true) : P.src[k];
+  }
+  for (int r = 0; r < gp.nred && r < kMaxRed; ++r) P.red_op[r] = ch.red_op[static_cast<size_t>(r)];
+  if (gp.nred > 0) P.red_partials = ensure_partials(static_cast<size_t>(gp.nred) * gp.ctas.size());
+  P.red_out = red_dev_;
+  const int64_t smem = static_cast<int64_t>(P.smem_doubles) * 8 + static_cast<int64_t>(gp.nloops) * (sizeof(DevLoop) + kMaxArgs * 16) +
+                       static_cast<int64_t>(gp.nred) * kTiledThreads * 8;
+  if (smem > info_.smem_optin) throw PlanError("tiled executor: shared memory request exceeds the device limit");
+  const dim3 grid(static_cast<unsigned>(gp.ctas.size())), block(kTiledThreads);
+  if (gp.dim == 1) {
+    set_tiled_smem<1>(smem);
+    tiled::k_tiled<1><<<grid, block, smem, st>>>(P);
+  } else if (gp.dim == 2) {
+    set_tiled_smem<2>(smem);
+    tiled::k_tiled<2><<<grid, block, smem, st>>>(P);
+  } else {
+    set_tiled_smem<3>(smem);
+    tiled::k_tiled<3><<<grid, block, smem, st>>>(P);
+  }
+  TCG_CK(cudaGetLastError());
+  ++launches_;
+  for (int k = 0; k < gp.ndat; ++k)
+    if (gp.dats[static_cast<size_t>(k)].pingpong) swap(gp.dat_ids[static_cast<size_t>(k)]);
+  for (int r = 0; r < gp.nred; ++r) {
+    k_fold<<<1, 1024, 0, st>>>(P.red_partials + static_cast<int64_t>(r) * P.nctas, P.nctas, P.red_op[r], red_dev_ + r);
+    TCG_CK(cudaGetLastError());
+    ++launches_;
+  }
+  if (gp.nred > 0) {
+    TCG_CK(cudaMemcpyAsync(red_out, red_dev_, sizeof(double) * static_cast<size_t>(gp.nred), cudaMemcpyDeviceToHost, st));
+    TCG_CK(cudaStreamSynchronize(st));
+  }
+}
+
+}  // namespace tcg

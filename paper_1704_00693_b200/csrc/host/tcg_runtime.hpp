@@ -1,0 +1,149 @@
+// Front door of the B200 stencil-chain executor: the reference's Runtime API
+// (proj/core/include/tilechain/runtime.hpp:44-135) with the same lazy-queue
+// semantics, rebuilt over device-resident fields and the CUDA executors.
+//   declare_stencil / declare_field        runtime.cpp:16-33 (pad rule kept)
+//   par_loop (validation, lazy enqueue)    runtime.cpp:35-92
+//   take_pending / flush / execute_chain   runtime.cpp:94-151
+//   fetch_reduction (prefix flush)         runtime.cpp:164-197
+//   get / put / fill_logical               runtime.cpp:199-212
+// Differences by design: fields live in HBM (the host never holds a copy),
+// kernels are registry bodies, and ExecMode::tiled / tiled_auto run the
+// windowed CTA executor.
+#pragma once
+#include <map>
+#include <memory>
+
+#include "tcg_exec.hpp"
+#include "tcg_gpuplan.hpp"
+#include "tcg_plan.hpp"
+
+namespace tcg {
+
+struct RuntimeConfig {
+  int threads = 1;                          // kept for API parity (CPU sizer input)
+  int64_t skew_allowance = 16;              // runtime.hpp:17
+  int64_t cache_bytes = int64_t{8} << 20;   // runtime.hpp:19 (reference sizer only)
+  bool flush_whole_queue_on_fetch = false;  // runtime.hpp:22
+  int stream_segments = 0;                  // GPU: CTA segments along the stream dim (0 = auto)
+};
+
+struct ExecMode {
+  enum class Kind : uint8_t { Untiled = 0, Tiled = 1, TiledAuto = 2 };
+  Kind kind = Kind::Untiled;
+  std::array<int64_t, kMaxDims> tile_sizes{0, 0, 0};
+  static ExecMode untiled() { return {}; }
+  static ExecMode tiled(const std::array<int64_t, kMaxDims>& ts) { return {Kind::Tiled, ts}; }
+  static ExecMode tiled_auto() { return {Kind::TiledAuto, {0, 0, 0}}; }
+};
+
+struct LoopExecStats {
+  int32_t loop_id = 0;
+  int64_t points = 0;
+  int64_t bytes_moved = 0;
+};
+
+// executor.hpp:57-80 plus the GPU plan shape.
+struct ExecutionReport {
+  bool tiled = false;
+  bool distributed = false;
+  bool plan_cache_hit = false;
+  int dim = 1;
+  std::array<int64_t, kMaxDims> tile_sizes{0, 0, 0};
+  std::array<int64_t, kMaxDims> max_skew{0, 0, 0};
+  int64_t tiles_executed = 0;
+  int64_t plan_constructions = 0;
+  double plan_seconds = 0;
+  double exec_seconds = 0;
+  double total_seconds = 0;
+  std::vector<LoopExecStats> loops;
+  int64_t halo_messages = 0, halo_bytes = 0, halo_exchanges = 0;
+  // GPU specifics
+  int64_t launches = 0;
+  int64_t ctas = 0;
+  int64_t subchains = 0;
+  int64_t computed_points = 0;
+  std::array<int, kMaxDims> cta_grid{1, 1, 1};
+  int64_t total_points() const;
+  int64_t total_bytes_moved() const;
+  std::string to_text() const;
+};
+
+class Runtime {
+ public:
+  Runtime(int dim, RuntimeConfig cfg = {});
+  ~Runtime();
+
+  StencilId declare_stencil(const std::string& name, std::vector<Point> offsets);
+  DatasetId declare_field(const std::string& name, const Range& logical, int elem_bytes = 8);
+
+  ReductionHandle par_loop(KernelHandle kernel, const Range& range, std::vector<ArgSpec> args,
+                           std::optional<ReduceOp> reduction = std::nullopt);
+
+  ExecutionReport flush(const ExecMode& mode);
+  ExecutionReport flush() { return flush(default_mode_); }
+  void set_default_mode(const ExecMode& m) { default_mode_ = m; }
+  const ExecMode& default_mode() const { return default_mode_; }
+
+  double fetch_reduction(ReductionHandle h);
+
+  double get(DatasetId ds, const Point& p);
+  void put(DatasetId ds, const Point& p, double v);
+  void fill_logical(DatasetId ds, double v);
+  // Bulk host <-> device copies of a whole allocation (dense, dim 0 fastest,
+  // the reference Field layout, field.cpp:22-26). Flush first.
+  void upload(DatasetId ds, const double* host);
+  void download(DatasetId ds, double* host);
+
+  size_t pending_loops() const { return pending_.size(); }
+  LoopChain take_pending();
+  const Range& alloc_range(DatasetId ds) const { return fields_.at(static_cast<size_t>(ds)).alloc; }
+  const Range& logical_range(DatasetId ds) const { return fields_.at(static_cast<size_t>(ds)).logical; }
+  size_t num_fields() const { return fields_.size(); }
+  int dim() const { return dim_; }
+  const RuntimeConfig& config() const { return cfg_; }
+  const std::vector<Stencil>& stencils() const { return stencils_; }
+  const ExecutionReport& last_report() const { return last_report_; }
+  std::shared_ptr<const GpuTiledPlan> last_gpu_plan() const { return last_gpu_plan_; }
+  PlanCache& plan_cache() { return plan_cache_; }
+  int64_t gpu_plan_constructions() const { return gpu_plan_builds_; }
+  DeviceExec& device();
+  bool device_ready() const { return dev_ != nullptr; }
+  std::vector<FieldGeom> field_geoms() const;
+
+ private:
+  struct FieldRec {
+    std::string name;
+    Range logical, alloc;
+    int64_t pad = 0;
+    int dev = -1;
+  };
+  struct Slot {
+    ReduceOp op = ReduceOp::Sum;
+    double value = 0;
+    bool ready = false;
+    bool consumed = false;
+  };
+
+  ExecutionReport execute_chain(LoopChain chain, const ExecMode& mode);
+  void ensure_fields();
+  DevChain lower(const LoopChain& chain, std::vector<ReductionHandle>& handles) const;
+  void run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep);
+  void store(const std::vector<ReductionHandle>& handles, const double* vals);
+
+  int dim_;
+  RuntimeConfig cfg_;
+  std::vector<Stencil> stencils_;
+  int64_t max_reach_ = 0;
+  std::vector<FieldRec> fields_;
+  std::vector<LoopRecord> pending_;
+  ExecMode default_mode_;
+  std::vector<Slot> slots_;
+  PlanCache plan_cache_;
+  std::map<std::tuple<uint64_t, int64_t, int64_t, int64_t, int>, std::shared_ptr<const GpuTiledPlan>> gpu_plans_;
+  int64_t gpu_plan_builds_ = 0;
+  std::shared_ptr<const GpuTiledPlan> last_gpu_plan_;
+  ExecutionReport last_report_;
+  std::unique_ptr<DeviceExec> dev_;
+};
+
+}  // namespace tcg

@@ -1,0 +1,342 @@
+// C-ABI boundary (include/tilechain_b200.h): plain pointers and sizes in,
+// status codes out; every C++ exception is translated to its TCG_ERR_* code.
+#include "../../include/tilechain_b200.h"
+
+#include <cstring>
+#include <sstream>
+
+#include "host/tcg_runtime.hpp"
+#include "kernels/tc_bodies.h"
+
+struct tcg_runtime {
+  std::unique_ptr<tcg::Runtime> rt;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return TCG_OK;
+  } catch (const tcg::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TCG_ERR_INTERNAL;
+  }
+}
+
+tcg::Range range6(int dim, const int64_t* r) { return tcg::Range::box(dim, r); }
+
+tcg::ExecMode mode_of(int mode, const int64_t* ts) {
+  if (mode == TCG_UNTILED) return tcg::ExecMode::untiled();
+  if (mode == TCG_TILED) return tcg::ExecMode::tiled({ts[0], ts[1], ts[2]});
+  if (mode == TCG_TILED_AUTO) return tcg::ExecMode::tiled_auto();
+  throw tcg::InvalidArgument("unknown exec mode " + std::to_string(mode));
+}
+
+void put_text(const std::string& s, char* buf, int64_t n, int64_t* needed) {
+  if (needed) *needed = static_cast<int64_t>(s.size()) + 1;
+  if (buf && n > 0) {
+    const size_t k = std::min<size_t>(static_cast<size_t>(n) - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+}
+
+std::string plan_text(const tcg::TilingPlan& p, int dim) {
+  std::ostringstream os;
+  os << p.dump() << "max_skew=";
+  for (int d = 0; d < dim; ++d) os << (d ? "," : "") << p.max_skew[d];
+  os << "\n";
+  for (const auto& [ds, r] : p.required) os << "required ds=" << ds << " " << r.to_string() << "\n";
+  return os.str();
+}
+
+std::string halo_text(const tcg::HaloSpec& h, int dim) {
+  std::ostringstream os;
+  for (const auto& [ds, e] : h.entries) {
+    os << "ds=" << ds << " needed=" << (e.needed ? 1 : 0);
+    for (int d = 0; d < dim; ++d) os << " d" << d << "=" << e.faces[d].lo << "," << e.faces[d].hi;
+    os << "\n";
+  }
+  return os.str();
+}
+
+// B200 constants for plan-only calls on a machine without a GPU.
+constexpr int kB200Sms = 148;
+constexpr int64_t kB200SmemOptin = 232448;
+
+}  // namespace
+
+extern "C" {
+
+size_t tcg_last_error(char* buf, size_t n) {
+  if (buf && n > 0) {
+    const size_t k = std::min(n - 1, g_err.size());
+    std::memcpy(buf, g_err.data(), k);
+    buf[k] = 0;
+  }
+  return g_err.size();
+}
+
+int tcg_abi_version(void) { return 1; }
+
+int tcg_runtime_new(int dim, const tcg_config* cfg, tcg_runtime** out) {
+  return guard([&] {
+    tcg::RuntimeConfig c;
+    if (cfg) {
+      c.threads = cfg->threads;
+      c.skew_allowance = cfg->skew_allowance;
+      c.cache_bytes = cfg->cache_bytes;
+      c.flush_whole_queue_on_fetch = cfg->flush_whole_queue_on_fetch != 0;
+      c.stream_segments = cfg->stream_segments;
+    }
+    auto* h = new tcg_runtime;
+    h->rt = std::make_unique<tcg::Runtime>(dim, c);
+    *out = h;
+  });
+}
+
+void tcg_runtime_free(tcg_runtime* rt) { delete rt; }
+
+int tcg_declare_stencil(tcg_runtime* rt, int npts, const int64_t* pts, int32_t* out_id) {
+  return guard([&] {
+    std::vector<tcg::Point> v;
+    for (int i = 0; i < npts; ++i) v.push_back(tcg::Point{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]});
+    *out_id = rt->rt->declare_stencil("", std::move(v));
+  });
+}
+
+int tcg_declare_field(tcg_runtime* rt, const char* name, const int64_t logical[6], int32_t* out_id) {
+  return guard([&] { *out_id = rt->rt->declare_field(name ? name : "", range6(rt->rt->dim(), logical)); });
+}
+
+int tcg_alloc_range(tcg_runtime* rt, int32_t ds, int64_t out[6]) {
+  return guard([&] {
+    if (ds < 0 || static_cast<size_t>(ds) >= rt->rt->num_fields()) throw tcg::InvalidArgument("unknown dataset");
+    const tcg::Range& a = rt->rt->alloc_range(ds);
+    for (int d = 0; d < 3; ++d) {
+      out[2 * d] = d < a.dim() ? a.start(d) : 0;
+      out[2 * d + 1] = d < a.dim() ? a.end(d) : 1;
+    }
+  });
+}
+
+int tcg_par_loop(tcg_runtime* rt, int32_t kernel_id, int32_t body, const int64_t range[6], int nargs,
+                 const int32_t* args, int red_op, int nparams, const double* params, int32_t* out_handle) {
+  return guard([&] {
+    tcg::KernelHandle k;
+    k.id = kernel_id;
+    k.name = "k" + std::to_string(kernel_id);
+    k.fn.body = body;
+    if (nparams > 0) k.fn.params.assign(params, params + nparams);
+    std::vector<tcg::ArgSpec> a;
+    for (int i = 0; i < nargs; ++i) {
+      if (args[3 * i + 2] < 0 || args[3 * i + 2] > 3) throw tcg::InvalidArgument("par_loop: bad access mode");
+      a.push_back(tcg::ArgSpec{args[3 * i], args[3 * i + 1], static_cast<tcg::AccessMode>(args[3 * i + 2])});
+    }
+    std::optional<tcg::ReduceOp> r;
+    if (red_op >= 0) {
+      if (red_op > 2) throw tcg::InvalidArgument("par_loop: bad reduction op");
+      r = static_cast<tcg::ReduceOp>(red_op);
+    }
+    const tcg::ReductionHandle h = rt->rt->par_loop(std::move(k), range6(rt->rt->dim(), range), std::move(a), r);
+    if (out_handle) *out_handle = h.id;
+  });
+}
+
+int tcg_flush(tcg_runtime* rt, int mode, const int64_t ts[3]) {
+  return guard([&] {
+    const int64_t z[3] = {0, 0, 0};
+    rt->rt->flush(mode_of(mode, ts ? ts : z));
+  });
+}
+
+int tcg_flush_default(tcg_runtime* rt) {
+  return guard([&] { rt->rt->flush(); });
+}
+
+int tcg_set_default_mode(tcg_runtime* rt, int mode, const int64_t ts[3]) {
+  return guard([&] {
+    const int64_t z[3] = {0, 0, 0};
+    rt->rt->set_default_mode(mode_of(mode, ts ? ts : z));
+  });
+}
+
+int tcg_fetch_reduction(tcg_runtime* rt, int32_t handle, double* out) {
+  return guard([&] { *out = rt->rt->fetch_reduction(tcg::ReductionHandle{handle}); });
+}
+
+int tcg_pending_loops(tcg_runtime* rt, int64_t* out) {
+  return guard([&] { *out = static_cast<int64_t>(rt->rt->pending_loops()); });
+}
+
+int tcg_get(tcg_runtime* rt, int32_t ds, const int64_t p[3], double* out) {
+  return guard([&] { *out = rt->rt->get(ds, tcg::Point{p[0], p[1], p[2]}); });
+}
+
+int tcg_put(tcg_runtime* rt, int32_t ds, const int64_t p[3], double v) {
+  return guard([&] { rt->rt->put(ds, tcg::Point{p[0], p[1], p[2]}, v); });
+}
+
+int tcg_fill_logical(tcg_runtime* rt, int32_t ds, double v) {
+  return guard([&] { rt->rt->fill_logical(ds, v); });
+}
+
+int tcg_upload(tcg_runtime* rt, int32_t ds, const double* host) {
+  return guard([&] {
+    if (ds < 0 || static_cast<size_t>(ds) >= rt->rt->num_fields()) throw tcg::InvalidArgument("unknown dataset");
+    rt->rt->upload(ds, host);
+  });
+}
+
+int tcg_download(tcg_runtime* rt, int32_t ds, double* host) {
+  return guard([&] {
+    if (ds < 0 || static_cast<size_t>(ds) >= rt->rt->num_fields()) throw tcg::InvalidArgument("unknown dataset");
+    rt->rt->download(ds, host);
+  });
+}
+
+int tcg_synchronize(tcg_runtime* rt) {
+  return guard([&] {
+    if (rt->rt->device_ready()) rt->rt->device().synchronize();
+  });
+}
+
+int tcg_report_text(tcg_runtime* rt, char* buf, int64_t n, int64_t* needed) {
+  return guard([&] { put_text(rt->rt->last_report().to_text(), buf, n, needed); });
+}
+
+int tcg_plan_pending(tcg_runtime* rt, const int64_t ts[3], char* buf, int64_t n, int64_t* needed) {
+  return guard([&] {
+    tcg::LoopChain c = rt->rt->take_pending();
+    const tcg::TilingPlan p = tcg::construct_plan(c, {ts[0], ts[1], ts[2]});
+    put_text(plan_text(p, c.dim), buf, n, needed);
+  });
+}
+
+int tcg_rank_plans_pending(tcg_runtime* rt, const int32_t grid[3], const int64_t ts[3], char* buf, int64_t n,
+                           int64_t* needed) {
+  return guard([&] {
+    tcg::LoopChain c = rt->rt->take_pending();
+    bool first = true;
+    tcg::Range global(c.dim);
+    for (size_t i = 0; i < rt->rt->num_fields(); ++i) {
+      const tcg::Range& l = rt->rt->logical_range(static_cast<tcg::DatasetId>(i));
+      global = first ? l : global.hull(l);
+      first = false;
+    }
+    const tcg::RankLayout lay = tcg::decompose(global, {grid[0], grid[1], grid[2]});
+    std::ostringstream os;
+    for (int r = 0; r < lay.rank_count(); ++r) {
+      const tcg::TilingPlan p = tcg::construct_rank_plan(c, lay, r, {ts[0], ts[1], ts[2]});
+      os << "rank=" << r << " owned=" << lay.owned[static_cast<size_t>(r)].to_string() << "\n";
+      os << plan_text(p, c.dim) << halo_text(tcg::compute_halo_depths(p, c, lay, r), c.dim);
+    }
+    put_text(os.str(), buf, n, needed);
+  });
+}
+
+int tcg_gpu_plan_pending(tcg_runtime* rt, int mode, const int64_t ts[3], char* buf, int64_t n, int64_t* needed) {
+  return guard([&] {
+    tcg::LoopChain c = rt->rt->take_pending();
+    const int s = c.dim - 1;
+    tcg::GpuTileChoice choice;
+    if (mode == TCG_TILED)
+      for (int d = 0; d < c.dim; ++d) {
+        if (d == s)
+          choice.stream_tile = std::max<int64_t>(1, ts[d]);
+        else
+          choice.block[d] = std::max<int64_t>(1, ts[d]);
+      }
+    choice.stream_segments = rt->rt->config().stream_segments;
+    int nred = 0;
+    for (const auto& l : c.loops) nred += l.reduction ? 1 : 0;
+    const int64_t fixed = 2048 + static_cast<int64_t>(c.size()) * static_cast<int64_t>(sizeof(tcg::DevLoop)) +
+                          static_cast<int64_t>(nred) * 512 * 8;
+    const int64_t budget = (kB200SmemOptin - fixed) / 8;
+    const tcg::GpuTiledPlan gp = tcg::build_gpu_tiled_plan(c, rt->rt->field_geoms(), choice, budget, kB200Sms);
+    std::ostringstream os;
+    os << "grid=" << gp.grid[0] << "," << gp.grid[1] << "," << gp.grid[2] << " block=" << gp.block[0] << ","
+       << gp.block[1] << " stream_tile=" << gp.stream_tile << " ctas=" << gp.ctas.size()
+       << " smem_doubles=" << gp.smem_doubles << " computed_points=" << gp.computed_points
+       << " recorded_points=" << gp.recorded_points << " max_skew=";
+    for (int d = 0; d < c.dim; ++d) os << (d ? "," : "") << gp.max_skew[d];
+    os << "\n";
+    for (int k = 0; k < gp.ndat; ++k)
+      os << "dat slot=" << k << " ds=" << gp.dat_ids[static_cast<size_t>(k)] << " load=" << gp.dats[static_cast<size_t>(k)].load
+         << " written=" << gp.dats[static_cast<size_t>(k)].written
+         << " pingpong=" << gp.dats[static_cast<size_t>(k)].pingpong << "\n";
+    for (size_t i = 0; i < gp.ctas.size(); ++i) {
+      const tcg::DevCta& ct = gp.ctas[i];
+      os << "cta=" << i << " ntiles=" << ct.ntiles << " own=";
+      for (int d = 0; d < c.dim; ++d) os << "[" << ct.own_lo[d] << "," << ct.own_hi[d] << ")";
+      os << " wb=";
+      for (int d = 0; d < c.dim; ++d) os << "[" << ct.wb_lo[d] << "," << ct.wb_hi[d] << ")";
+      os << " cols=[" << ct.col_lo[0] << "," << ct.col_hi[0] << ")[" << ct.col_lo[1] << "," << ct.col_hi[1] << ") W=";
+      for (int k = 0; k < gp.ndat; ++k) os << (k ? "," : "") << ct.W[k];
+      os << "\n";
+      for (int t = 0; t < ct.ntiles; ++t)
+        for (int l = 0; l < gp.nloops; ++l) {
+          const int32_t* b = &gp.boxes[static_cast<size_t>(ct.box_off) + (static_cast<size_t>(t) * gp.nloops + l) * 6];
+          os << "box cta=" << i << " tile=" << t << " loop=" << l;
+          for (int d = 0; d < c.dim; ++d) os << " [" << b[2 * d] << "," << b[2 * d + 1] << ")";
+          os << "\n";
+        }
+    }
+    put_text(os.str(), buf, n, needed);
+  });
+}
+
+int tcg_signature_pending(tcg_runtime* rt, uint64_t* out) {
+  return guard([&] {
+    tcg::LoopChain c = rt->rt->take_pending();
+    *out = c.signature();
+  });
+}
+
+int tcg_auto_tile_size(int dim, int64_t cache_bytes, int32_t threads, int64_t bpp, const int64_t extent[6],
+                       int64_t out[3]) {
+  return guard([&] {
+    tcg::SizerInput in;
+    in.dim = dim;
+    in.cache_bytes = cache_bytes;
+    in.threads = threads;
+    in.bytes_per_point = bpp;
+    in.domain_extent = tcg::Range::box(dim, extent);
+    const auto ts = tcg::auto_tile_size(in);
+    for (int d = 0; d < 3; ++d) out[d] = ts[d];
+  });
+}
+
+int tcg_device_info(char* name, size_t n, int32_t* num_sms, int64_t* smem_optin, int64_t* l2_bytes) {
+  return guard([&] {
+    tcg::DeviceExec ex;
+    const tcg::DeviceInfo& i = ex.info();
+    if (name && n > 0) {
+      const size_t k = std::min(n - 1, i.name.size());
+      std::memcpy(name, i.name.data(), k);
+      name[k] = 0;
+    }
+    if (num_sms) *num_sms = i.num_sms;
+    if (smem_optin) *smem_optin = i.smem_optin;
+    if (l2_bytes) *l2_bytes = i.l2_bytes;
+  });
+}
+
+int tcg_launches(tcg_runtime* rt, int64_t* out) {
+  return guard([&] { *out = rt->rt->device_ready() ? rt->rt->device().launches() : 0; });
+}
+
+int tcg_stream(tcg_runtime* rt, void** out) {
+  return guard([&] { *out = rt->rt->device().stream(); });
+}
+
+int tcg_body_known(int32_t body) { return tcb::body_known(body) ? 1 : 0; }
+
+}  // extern "C"

@@ -1,0 +1,423 @@
+"""Python mirror of the reference front door over the C-ABI (include/tilechain_b200.h).
+
+Names, argument meaning and error behaviour follow tilechain::Runtime
+(proj/core/include/tilechain/runtime.hpp:44-135) so tests read like the
+reference's own tests:
+
+    rt = Runtime(2)
+    five = rt.declare_stencil("five", [(0,0),(1,0),(-1,0),(0,1),(0,-1)])
+    a = rt.declare_field("a", Range.d2(0, 64, 0, 64))
+    h = rt.par_loop(KernelHandle(0, "jacobi", body=kernels.JACOBI_STENCIL), Range.d2(1, 63, 1, 63),
+                    [ArgSpec(a, five, AccessMode.Read), ArgSpec(b, ident, AccessMode.Write)])
+    rt.flush(ExecMode.tiled_auto())
+
+Every call goes through libtcg.so; there is no Python or CPU execution path.
+If the library or the GPU is missing the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_lib" / "libtcg.so"
+_lib: Optional[ctypes.CDLL] = None
+
+
+class TcgError(RuntimeError):
+    code = 6
+
+
+class InvalidArgument(TcgError):
+    code = 1
+
+
+class AccessError(TcgError):
+    code = 2
+
+
+class PlanError(TcgError):
+    code = 3
+
+
+class CudaError(TcgError):
+    code = 4
+
+
+class SizerError(TcgError):
+    code = 5
+
+
+_ERR = {1: InvalidArgument, 2: AccessError, 3: PlanError, 4: CudaError, 5: SizerError, 6: TcgError}
+
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("threads", _I32), ("skew_allowance", _I64), ("cache_bytes", _I64),
+                ("flush_whole_queue_on_fetch", _I32), ("stream_segments", _I32)]
+
+
+def load_library() -> ctypes.CDLL:
+    """Loads the in-tree executor library; raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    sig = {
+        "tcg_last_error": (ctypes.c_size_t, [ctypes.c_char_p, ctypes.c_size_t]),
+        "tcg_abi_version": (ctypes.c_int, []),
+        "tcg_runtime_new": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_Config), ctypes.POINTER(_P)]),
+        "tcg_runtime_free": (None, [_P]),
+        "tcg_declare_stencil": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
+        "tcg_declare_field": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
+        "tcg_alloc_range": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_I64)]),
+        "tcg_par_loop": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(_I64), ctypes.c_int, ctypes.POINTER(_I32),
+                                        ctypes.c_int, ctypes.c_int, ctypes.POINTER(_D), ctypes.POINTER(_I32)]),
+        "tcg_flush": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I64)]),
+        "tcg_flush_default": (ctypes.c_int, [_P]),
+        "tcg_set_default_mode": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I64)]),
+        "tcg_fetch_reduction": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_D)]),
+        "tcg_pending_loops": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
+        "tcg_get": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_D)]),
+        "tcg_put": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_I64), _D]),
+        "tcg_fill_logical": (ctypes.c_int, [_P, _I32, _D]),
+        "tcg_upload": (ctypes.c_int, [_P, _I32, _P]),
+        "tcg_download": (ctypes.c_int, [_P, _I32, _P]),
+        "tcg_synchronize": (ctypes.c_int, [_P]),
+        "tcg_report_text": (ctypes.c_int, [_P, ctypes.c_char_p, _I64, ctypes.POINTER(_I64)]),
+        "tcg_plan_pending": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.c_char_p, _I64, ctypes.POINTER(_I64)]),
+        "tcg_rank_plans_pending": (ctypes.c_int, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I64), ctypes.c_char_p, _I64,
+                                                  ctypes.POINTER(_I64)]),
+        "tcg_gpu_plan_pending": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I64), ctypes.c_char_p, _I64,
+                                                ctypes.POINTER(_I64)]),
+        "tcg_signature_pending": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
+        "tcg_auto_tile_size": (ctypes.c_int, [ctypes.c_int, _I64, _I32, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+        "tcg_device_info": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(_I32), ctypes.POINTER(_I64),
+                                           ctypes.POINTER(_I64)]),
+        "tcg_launches": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
+        "tcg_stream": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+        "tcg_body_known": (ctypes.c_int, [_I32]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        buf = ctypes.create_string_buffer(4096)
+        _lib.tcg_last_error(buf, 4096)
+        raise _ERR.get(rc, TcgError)(buf.value.decode(errors="replace"))
+
+
+def _arr(ctype, vals):
+    vals = list(vals)
+    return (ctype * max(1, len(vals)))(*vals)
+
+
+def _text(fn, *args, size: int = 1 << 22) -> str:
+    # One call only: several of these consume the pending queue.
+    need = _I64(0)
+    buf = ctypes.create_string_buffer(size)
+    _check(fn(*args, buf, len(buf), ctypes.byref(need)))
+    if need.value > size:
+        raise TcgError(f"text output truncated ({need.value} bytes > {size}); pass a larger size")
+    return buf.value.decode()
+
+
+class AccessMode(enum.IntEnum):
+    Read = 0
+    Write = 1
+    ReadWrite = 2
+    Increment = 3
+
+
+class ReduceOp(enum.IntEnum):
+    Sum = 0
+    Min = 1
+    Max = 2
+
+
+class Range:
+    """Half-open box per dimension (types.hpp:46-183)."""
+
+    def __init__(self, dim: int, lohi: Sequence[int]):
+        if dim < 1 or dim > 3:
+            raise InvalidArgument("Range: dim must be 1, 2, or 3")
+        self.dim = dim
+        self.lohi = [int(v) for v in lohi[: 2 * dim]] + [0, 1] * (3 - dim)
+
+    @staticmethod
+    def d1(s0, e0):
+        return Range(1, [s0, e0])
+
+    @staticmethod
+    def d2(s0, e0, s1, e1):
+        return Range(2, [s0, e0, s1, e1])
+
+    @staticmethod
+    def d3(s0, e0, s1, e1, s2, e2):
+        return Range(3, [s0, e0, s1, e1, s2, e2])
+
+    def start(self, d):
+        return self.lohi[2 * d]
+
+    def end(self, d):
+        return self.lohi[2 * d + 1]
+
+    def extent(self, d):
+        return self.end(d) - self.start(d)
+
+    def volume(self) -> int:
+        v = 1
+        for d in range(self.dim):
+            v *= max(0, self.extent(d))
+        return v
+
+    def shape(self):
+        """numpy shape of a dense array over this box (dim 0 fastest)."""
+        return tuple(self.extent(d) for d in reversed(range(self.dim)))
+
+    def __eq__(self, o):
+        return isinstance(o, Range) and self.dim == o.dim and self.lohi[: 2 * self.dim] == o.lohi[: 2 * o.dim]
+
+    def __repr__(self):
+        return "x".join(f"[{self.start(d)},{self.end(d)})" for d in range(self.dim))
+
+
+@dataclass
+class ArgSpec:
+    dataset: int
+    stencil: int
+    mode: AccessMode = AccessMode.Read
+
+
+@dataclass
+class KernelHandle:
+    """Reference KernelHandle{id, name, fn}: `body` + `params` replace the closure."""
+
+    id: int
+    name: str
+    body: int
+    params: Sequence[float] = field(default_factory=tuple)
+
+
+@dataclass
+class ExecMode:
+    kind: int = 0
+    tile_sizes: Sequence[int] = (0, 0, 0)
+
+    @staticmethod
+    def untiled():
+        return ExecMode(0, (0, 0, 0))
+
+    @staticmethod
+    def tiled(ts):
+        ts = list(ts) + [1] * (3 - len(ts))
+        return ExecMode(1, tuple(int(v) for v in ts[:3]))
+
+    @staticmethod
+    def tiled_auto():
+        return ExecMode(2, (0, 0, 0))
+
+
+@dataclass
+class RuntimeConfig:
+    threads: int = 1
+    skew_allowance: int = 16
+    cache_bytes: int = 8 << 20
+    flush_whole_queue_on_fetch: bool = False
+    stream_segments: int = 0
+
+
+def parse_report(text: str) -> dict:
+    rep = {}
+    for line in text.splitlines():
+        if "=" in line:
+            k, v = line.split("=", 1)
+            rep[k] = v
+    return rep
+
+
+class Runtime:
+    """tilechain::Runtime over the B200 executor."""
+
+    def __init__(self, dim: int, config: Optional[RuntimeConfig] = None):
+        lib = load_library()
+        cfg = config or RuntimeConfig()
+        c = _Config(cfg.threads, cfg.skew_allowance, cfg.cache_bytes, int(cfg.flush_whole_queue_on_fetch),
+                    cfg.stream_segments)
+        h = _P()
+        _check(lib.tcg_runtime_new(dim, ctypes.byref(c), ctypes.byref(h)))
+        self._h = h
+        self._lib = lib
+        self.dim = dim
+        self.config = cfg
+        self._allocs: list[Range] = []
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.tcg_runtime_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- declarations --------------------------------------------------
+    def declare_stencil(self, name: str, points: Iterable[Sequence[int]]) -> int:
+        flat = []
+        n = 0
+        for p in points:
+            p = list(p) + [0] * (3 - len(p))
+            flat += p[:3]
+            n += 1
+        out = _I32()
+        _check(self._lib.tcg_declare_stencil(self._h, n, _arr(_I64, flat), ctypes.byref(out)))
+        return out.value
+
+    def declare_field(self, name: str, logical: Range, elem_bytes: int = 8) -> int:
+        if elem_bytes != 8:
+            raise InvalidArgument("declare_field: the B200 executor stores fp64 (elem_bytes = 8)")
+        out = _I32()
+        _check(self._lib.tcg_declare_field(self._h, name.encode(), _arr(_I64, logical.lohi), ctypes.byref(out)))
+        a = (_I64 * 6)()
+        _check(self._lib.tcg_alloc_range(self._h, out.value, a))
+        self._allocs.append(Range(self.dim, list(a)))
+        return out.value
+
+    def alloc_range(self, ds: int) -> Range:
+        return self._allocs[ds]
+
+    # ---- lazy queue -----------------------------------------------------
+    def par_loop(self, kernel: KernelHandle, rng: Range, args: Sequence, reduction: Optional[int] = None) -> int:
+        if rng.dim != self.dim:
+            raise InvalidArgument("par_loop: range dim does not match block")
+        flat = []
+        for a in args:
+            if isinstance(a, ArgSpec):
+                flat += [a.dataset, a.stencil, int(a.mode)]
+            else:
+                flat += [int(a[0]), int(a[1]), int(a[2])]
+        prm = list(kernel.params)
+        out = _I32(-1)
+        _check(self._lib.tcg_par_loop(self._h, kernel.id, kernel.body, _arr(_I64, rng.lohi), len(args),
+                                      _arr(_I32, flat), -1 if reduction is None else int(reduction), len(prm),
+                                      _arr(_D, prm), ctypes.byref(out)))
+        return out.value
+
+    def flush(self, mode: Optional[ExecMode] = None) -> dict:
+        if mode is None:
+            _check(self._lib.tcg_flush_default(self._h))
+        else:
+            _check(self._lib.tcg_flush(self._h, mode.kind, _arr(_I64, mode.tile_sizes)))
+        return parse_report(self.report_text())
+
+    def set_default_mode(self, mode: ExecMode) -> None:
+        _check(self._lib.tcg_set_default_mode(self._h, mode.kind, _arr(_I64, mode.tile_sizes)))
+
+    def fetch_reduction(self, handle: int) -> float:
+        out = _D()
+        _check(self._lib.tcg_fetch_reduction(self._h, handle, ctypes.byref(out)))
+        return out.value
+
+    def pending_loops(self) -> int:
+        out = _I64()
+        _check(self._lib.tcg_pending_loops(self._h, ctypes.byref(out)))
+        return out.value
+
+    # ---- host access --------------------------------------------------------
+    def get(self, ds: int, p: Sequence[int]) -> float:
+        p = list(p) + [0] * (3 - len(p))
+        out = _D()
+        _check(self._lib.tcg_get(self._h, ds, _arr(_I64, p[:3]), ctypes.byref(out)))
+        return out.value
+
+    def put(self, ds: int, p: Sequence[int], v: float) -> None:
+        p = list(p) + [0] * (3 - len(p))
+        _check(self._lib.tcg_put(self._h, ds, _arr(_I64, p[:3]), float(v)))
+
+    def fill_logical(self, ds: int, v: float) -> None:
+        _check(self._lib.tcg_fill_logical(self._h, ds, float(v)))
+
+    def upload(self, ds: int, data: np.ndarray) -> None:
+        a = self._allocs[ds]
+        arr = np.ascontiguousarray(data, dtype=np.float64)
+        if arr.size != a.volume():
+            raise InvalidArgument(f"upload: expected {a.volume()} values for {a}, got {arr.size}")
+        _check(self._lib.tcg_upload(self._h, ds, arr.ctypes.data_as(_P)))
+
+    def download(self, ds: int) -> np.ndarray:
+        a = self._allocs[ds]
+        out = np.empty(a.shape(), dtype=np.float64)
+        _check(self._lib.tcg_download(self._h, ds, out.ctypes.data_as(_P)))
+        return out
+
+    def synchronize(self) -> None:
+        _check(self._lib.tcg_synchronize(self._h))
+
+    # ---- introspection ------------------------------------------------------
+    def report_text(self) -> str:
+        return _text(self._lib.tcg_report_text, self._h)
+
+    def plan_pending(self, tile_sizes) -> str:
+        ts = list(tile_sizes) + [0] * (3 - len(tile_sizes))
+        return _text(self._lib.tcg_plan_pending, self._h, _arr(_I64, ts[:3]))
+
+    def rank_plans_pending(self, grid, tile_sizes) -> str:
+        g = list(grid) + [1] * (3 - len(grid))
+        ts = list(tile_sizes) + [0] * (3 - len(tile_sizes))
+        return _text(self._lib.tcg_rank_plans_pending, self._h, _arr(_I32, g[:3]), _arr(_I64, ts[:3]))
+
+    def gpu_plan_pending(self, mode: ExecMode, size: int = 1 << 26) -> str:
+        return _text(self._lib.tcg_gpu_plan_pending, self._h, mode.kind, _arr(_I64, mode.tile_sizes), size=size)
+
+    def signature_pending(self) -> int:
+        out = ctypes.c_uint64()
+        _check(self._lib.tcg_signature_pending(self._h, ctypes.byref(out)))
+        return out.value
+
+    def launches(self) -> int:
+        out = _I64()
+        _check(self._lib.tcg_launches(self._h, ctypes.byref(out)))
+        return out.value
+
+    def stream(self) -> int:
+        out = _P()
+        _check(self._lib.tcg_stream(self._h, ctypes.byref(out)))
+        return out.value or 0
+
+
+def auto_tile_size(dim, cache_bytes, threads, bytes_per_point, extent: Range):
+    lib = load_library()
+    out = (_I64 * 3)()
+    _check(lib.tcg_auto_tile_size(dim, cache_bytes, threads, bytes_per_point, _arr(_I64, extent.lohi), out))
+    return tuple(out)
+
+
+def device_info() -> dict:
+    lib = load_library()
+    name = ctypes.create_string_buffer(256)
+    sms, smem, l2 = _I32(), _I64(), _I64()
+    _check(lib.tcg_device_info(name, 256, ctypes.byref(sms), ctypes.byref(smem), ctypes.byref(l2)))
+    return {"name": name.value.decode(), "num_sms": sms.value, "smem_optin": smem.value, "l2_bytes": l2.value}
+
+
+def body_known(body: int) -> bool:
+    return bool(load_library().tcg_body_known(body))

@@ -1,0 +1,145 @@
+"""GPU parity: the B200 executors (untiled and windowed-tiled) against the
+sequential oracle and the unmodified reference, through the C-ABI.
+
+Bar (BASELINE north_star): per-point fp64 arithmetic bit-exact (-fmad=false on
+the device, FMA-free host oracle); Sum reductions within 1e-12 relative of the
+oracle's visit-order sum (the reference's own tolerance across thread counts,
+test_executor.cpp:117-142); Min/Max exact."""
+import numpy as np
+import pytest
+
+import chains as C
+from paper_1704_00693_b200 import ExecMode, Runtime, RuntimeConfig, configs
+
+pytestmark = pytest.mark.gpu
+
+MODES = {
+    "untiled": lambda dim, seed: ExecMode.untiled(),
+    "tiled": lambda dim, seed: ExecMode.tiled(C.random_tile_sizes(seed, dim)),
+    "auto": lambda dim, seed: ExecMode.tiled_auto(),
+}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("dim,seeds,kw", [
+    (2, range(1, 41), {}),
+    (1, range(5001, 5021), {"extent": (32, 96)}),
+    (3, range(9001, 9013), {"extent": (8, 16)}),
+])
+def test_random_chains_match_oracle(oracle_lib, mode, dim, seeds, kw):
+    for seed in seeds:
+        gc = C.generate(seed, dim=dim, **kw)
+        want = C.run(oracle_lib.OracleRuntime(dim), gc, None)
+        got = C.run(Runtime(dim), gc, MODES[mode](dim, seed))
+        C.assert_same(got, want, f"{mode} dim{dim} seed{seed}")
+
+
+@pytest.mark.parametrize("segments", [1, 3])
+def test_random_chains_stream_segments(oracle_lib, segments):
+    # CTA segments along the stream dimension exercise the left-extension
+    # (has_left) path of the rank plan (dist.cpp:300-310).
+    for seed in range(101, 121):
+        gc = C.generate(seed, dim=2)
+        want = C.run(oracle_lib.OracleRuntime(2), gc, None)
+        got = C.run(Runtime(2, RuntimeConfig(stream_segments=segments)), gc,
+                    ExecMode.tiled(C.random_tile_sizes(seed, 2)))
+        C.assert_same(got, want, f"segments{segments} seed{seed}")
+
+
+@pytest.mark.parametrize("copy", [True, False])
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((16, 16, 1)), ExecMode.tiled((8, 4, 1)),
+                                  ExecMode.tiled_auto()])
+def test_jacobi_app_matches_reference_app(ref_lib, copy, mode):
+    want = ref_lib.ref_app_jacobi(64, 64, 10, copy)
+    rt = Runtime(2)
+    j = configs.Jacobi2D(rt, 64, 64)
+    j.enqueue(10, copy)
+    rt.flush(mode)
+    got = np.stack([j.logical(j.a), j.logical(j.b)])
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((8, 8, 1)), ExecMode.tiled((48, 16, 1)),
+                                  ExecMode.tiled_auto()])
+def test_minihydro_app_matches_reference_app(ref_lib, mode):
+    fields, monitors = ref_lib.ref_app_minihydro(48, 48, 3)
+    rt = Runtime(2)
+    rt.set_default_mode(mode)
+    m = configs.MiniHydro(rt, 48, 48)
+    got_mon = m.run(3)
+    got = np.stack([m.logical(n) for n in ["rho", "e", "p", "u", "v", "fx", "fy", "w"]])
+    assert np.array_equal(got, fields)
+    for a, b in zip(got_mon, monitors):
+        assert abs(a - b) <= 1e-12 * max(1.0, abs(b))
+
+
+def _run_config(rt, cfg_cls, n, **kw):
+    c = cfg_cls(rt, n)
+    if cfg_cls is configs.HeatC1:
+        for _ in range(kw.get("chains", 2)):
+            c.enqueue_chain()
+            rt.flush(kw.get("mode"))
+        return c.outputs(), []
+    if cfg_cls is configs.HydroC2:
+        rt.set_default_mode(kw.get("mode") or ExecMode.untiled())
+        mins = [rt.fetch_reduction(c.enqueue_step()) for _ in range(kw.get("steps", 3))]
+        return c.outputs(), mins
+    if cfg_cls is configs.Jacobi3DC3:
+        c.enqueue_chain()
+        rt.flush(kw.get("mode"))
+        return c.outputs(), []
+    raise ValueError(cfg_cls)
+
+
+@pytest.mark.parametrize("cfg,n", [(configs.HeatC1, 64), (configs.HydroC2, 96), (configs.Jacobi3DC3, 24)])
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled_auto()])
+def test_configs_small_match_oracle(oracle_lib, cfg, n, mode):
+    want = _run_config(oracle_lib.OracleRuntime(3 if cfg is configs.Jacobi3DC3 else 2), cfg, n)
+    got = _run_config(Runtime(3 if cfg is configs.Jacobi3DC3 else 2), cfg, n, mode=mode)
+    for k in want[0]:
+        assert np.array_equal(got[0][k], want[0][k]), k
+    assert got[1] == want[1]
+
+
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled_auto()])
+def test_cg_residual_history_matches_reference(ref_lib, mode):
+    # c4 at 64^2: the residual history must agree to 1e-10 relative over the
+    # window where the reference is self-consistent (SURVEY.md §7 hard parts).
+    iters = 30
+    ref = ref_lib.RefRuntime(2)
+    cr = configs.CgC4(ref, 64)
+    cr.start()
+    for _ in range(iters):
+        cr.iterate()
+    rt = Runtime(2)
+    rt.set_default_mode(mode)
+    cg = configs.CgC4(rt, 64)
+    cg.start()
+    for _ in range(iters):
+        cg.iterate()
+    h, w = np.array(cg.history), np.array(cr.history)
+    rel = np.abs(h - w) / np.maximum(np.abs(w), 1e-300)
+    assert rel.max() <= 1e-10, rel
+
+
+def test_fetch_reduction_flushes_prefix_only():
+    from paper_1704_00693_b200 import ArgSpec, AccessMode, KernelHandle, Range, ReduceOp, kernels
+    rt = Runtime(1)
+    ident = rt.declare_stencil("id", [(0,)])
+    f0 = rt.declare_field("f0", Range.d1(0, 8))
+    f1 = rt.declare_field("f1", Range.d1(0, 8))
+    rt.par_loop(KernelHandle(0, "iota", kernels.IOTA), Range.d1(0, 8), [ArgSpec(f0, ident, AccessMode.Write)])
+    h = rt.par_loop(KernelHandle(1, "sum", kernels.SUM_READ), Range.d1(0, 8), [ArgSpec(f0, ident, AccessMode.Read)],
+                    ReduceOp.Sum)
+    rt.par_loop(KernelHandle(2, "copy", kernels.COPY), Range.d1(0, 8),
+                [ArgSpec(f0, ident, AccessMode.Read), ArgSpec(f1, ident, AccessMode.Write)])
+    assert rt.fetch_reduction(h) == 28.0
+    assert rt.pending_loops() == 1
+    with pytest.raises(Exception):
+        rt.fetch_reduction(h)
+    assert rt.get(f1, (5,)) == 5.0
+    assert rt.pending_loops() == 0
+    rt.put(f1, (5,), 2.5)
+    assert rt.get(f1, (5,)) == 2.5
+    rt.fill_logical(f1, 1.5)
+    assert rt.get(f1, (0,)) == 1.5 and rt.get(f1, (-1,)) == 0.0
