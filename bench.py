@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 lazy stencil-chain executor (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c2|c1|c3|c4] [--mode auto|untiled|tiled:X,Y,Z]
+
+Workload (N=1): BASELINE.json configs[1], the c2 2D hydro-like chain at
+4096^2 fp64 (8 datasets, 12 stencil loops + 1 min-reduction per step, one
+chain per step closed by fetch_reduction). A step = one timestep of that
+chain. Metric: cell-updates/s (one loop applied at one point of its recorded
+range, bench_jacobi.cpp:26). Inputs (8 x 134 MB) exceed the 126 MB L2, so no
+L2 flush is needed between steps.
+
+value   device-resident whole-job throughput: K steps timed with CUDA events on
+        the executor stream, max over ranks.
+e2e     same metric through the public API with HOST buffers: the job uploads
+        the 8 fields from pinned host memory, runs K steps (each step's
+        min-reduction read back to the host), downloads the 8 fields; all
+        copies inside the timed region.
+--impl reference: the unmodified reference tilechain library
+        (oracle/_ref/libtcref.so) on the host cores, same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "stencil-chain cell-updates/s"
+UNIT = "cell-updates/s"
+
+
+def load_peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_profile_traffic(key):
+    p = REPO / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(key)
+    return None
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons via NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_config(name, rt, n=None):
+    from paper_1704_00693_b200 import configs
+    if name == "c2":
+        return configs.HydroC2(rt, n or 4096)
+    if name == "c1":
+        return configs.HeatC1(rt, n or 1024)
+    if name == "c3":
+        return configs.Jacobi3DC3(rt, n or 512)
+    if name == "c4":
+        return configs.CgC4(rt, n or 4096)
+    raise ValueError(name)
+
+
+class Step:
+    """One 'step' of each config through the Runtime API."""
+
+    def __init__(self, name, cfg, rt):
+        self.name, self.cfg, self.rt = name, cfg, rt
+        if name == "c4":
+            cfg.start()
+
+    def __call__(self):
+        c, rt = self.cfg, self.rt
+        if self.name == "c2":
+            rt.fetch_reduction(c.enqueue_step())
+        elif self.name in ("c1", "c3"):
+            c.enqueue_chain()
+            rt.flush()
+        elif self.name == "c4":
+            c.iterate()
+
+    def cell_updates(self):
+        c = self.cfg
+        return {"c2": lambda: c.cell_updates_per_step(), "c1": lambda: c.cell_updates_per_chain(),
+                "c3": lambda: c.cell_updates_per_chain(), "c4": lambda: c.cell_updates_per_iteration()}[self.name]()
+
+    def algorithmic_bytes(self):
+        c = self.cfg
+        return {"c2": lambda: c.bytes_per_step(), "c1": lambda: c.bytes_per_chain(), "c3": lambda: c.bytes_per_chain(),
+                "c4": lambda: c.bytes_per_iteration()}[self.name]()
+
+    def compulsory_bytes(self):
+        """Bytes a perfectly fused chain must move: each seeded dataset read
+        once, each written dataset written once (over the recorded domain)."""
+        c = self.cfg
+        if self.name == "c2":
+            return 16 * 8 * c.n * c.n
+        if self.name == "c1":
+            return 3 * 8 * c.n * c.n
+        if self.name == "c3":
+            return 3 * 8 * c.inner.volume()
+        return 4 * 8 * c.n * c.n * 4 // 2
+
+
+WORKLOAD_TEXT = {
+    "c2": "c2_hydro2d: fp64 4096^2, 8 dats U[0.5,1.5) seed 7, 12 stencil loops (point/star5/box9/one-sided/star2) "
+          "+ min-reduction per step, one chain per step closed by fetch_reduction",
+    "c1": "c1_heat2d: fp64 1024^2, u U[0,1) seed 42, 20-loop chains (10 timesteps of lap + copy)",
+    "c3": "c3_jacobi3d: fp64 512^3, 16-loop chains (8 sweeps a->b->a)",
+    "c4": "c4_cg2d: fp64 4096^2 CG, 4 loops + 2 dot reductions per iteration",
+}
+
+
+def parse_mode(s):
+    from paper_1704_00693_b200 import ExecMode
+    if s == "auto":
+        return ExecMode.tiled_auto()
+    if s == "untiled":
+        return ExecMode.untiled()
+    if s.startswith("tiled:"):
+        return ExecMode.tiled([int(v) for v in s[6:].split(",")])
+    raise ValueError(s)
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = td
+    return world, rank, local, dist
+
+
+def max_over_ranks(v, dist):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def time_steps(rt, step, k):
+    """Device time of k steps on the executor stream (CUDA events)."""
+    import torch
+    stream = torch.cuda.ExternalStream(rt.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rt.synchronize()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(k):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    rt.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def cpu_reference(cfg_name, k, warmup, budget_s=120.0, mode_pick=None):
+    """The unmodified reference (oracle/_ref) on the host cores: best of its
+    untiled and tiled_auto modes, a bounded number of steps."""
+    sys.path.insert(0, str(REPO / "oracle"))
+    import pyoracle
+    from paper_1704_00693_b200 import ExecMode
+    if not pyoracle.ref_available():
+        return None, "reference library oracle/_ref/libtcref.so not built"
+    threads = os.cpu_count() or 1
+    best = None
+    modes = [("untiled", ExecMode.untiled()), ("tiled_auto", ExecMode.tiled_auto())]
+    if mode_pick:
+        modes = [m for m in modes if m[0] == mode_pick]
+    for mname, mode in modes:
+        rt = pyoracle.RefRuntime(2 if cfg_name != "c3" else 3, threads=threads)
+        rt.set_default_mode(mode)
+        cfg = make_config(cfg_name, rt)
+        st = Step(cfg_name, cfg, rt)
+        t0 = time.perf_counter()
+        st()  # probe step (also warm-up)
+        t_step = time.perf_counter() - t0
+        n = max(1, min(k, int(budget_s / max(t_step, 1e-3) / len(modes))))
+        t0 = time.perf_counter()
+        for _ in range(n):
+            st()
+        dt = time.perf_counter() - t0
+        v = st.cell_updates() * n / dt
+        if best is None or v > best[0]:
+            best = (v, mname, n, dt)
+        del rt
+    v, mname, n, dt = best
+    return {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{n} full {cfg_name} steps at BASELINE size ({dt:.1f} s), reference tilechain "
+                      f"RuntimeConfig.threads={threads}, best of untiled/tiled_auto = {mname}"}, None
+
+
+def run_reference_arm(args, world, rank, dist):
+    if rank != 0:
+        return 0
+    res, err = cpu_reference(args.config, args.steps + args.warmup, args.warmup, budget_s=args.ref_budget)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": err}))
+        return 0
+    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE shapes)",
+            "config": {"workload": WORKLOAD_TEXT[args.config]}, "impl": "reference", "cpu_baseline": res,
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--mode", default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-untiled", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=60.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world, rank, local, dist = dist_setup(args.gpus)
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank, dist)
+
+    import torch
+    import paper_1704_00693_b200 as pkg
+    from paper_1704_00693_b200 import Runtime
+
+    pkg.runtime.select_device(local)
+    torch.cuda.set_device(local)
+    mode = parse_mode(args.mode)
+
+    def build(m):
+        rt = Runtime(3 if args.config == "c3" else 2)
+        rt.set_default_mode(m)
+        cfg = make_config(args.config, rt)
+        return rt, cfg, Step(args.config, cfg, rt)
+
+    # ---- device-resident throughput (value) ----------------------------------
+    rt, cfg, step = build(mode)
+    for _ in range(args.warmup):
+        step()
+    barrier(dist)
+    rt.set_timing(True)
+    l0 = rt.launches()
+    with ClockSampler(local) as clk:
+        ms = time_steps(rt, step, args.steps)
+    launches = rt.launches() - l0
+    kt = rt.kernel_timing()
+    rt.set_timing(False)
+    ms = max_over_ranks(ms, dist)
+    cu = step.cell_updates()
+    value = cu * args.steps * world / (ms / 1e3)
+    report = pkg.parse_report(rt.report_text())
+
+    tiled = mode.kind != 0
+    kname = "k_tiled" if tiled else "k_untiled"
+    kms = kt["tiled_ms"] if tiled else kt["untiled_ms"]
+    kn = kt["tiled_launches"] if tiled else kt["untiled_launches"]
+    peak, peak_src = load_peaks()
+    alg = step.algorithmic_bytes()
+    comp = step.compulsory_bytes()
+    per_launch_alg = alg * args.steps / max(kn, 1)
+    avg_ms = kms / max(kn, 1)
+    achieved = per_launch_alg / (avg_ms / 1e3) / 1e9 if kn else None
+    traffic = load_profile_traffic(f"{args.config}_{kname}")
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": per_launch_alg,
+                "avg_launch_ms": avg_ms, "launches": kn, "kernel_share_of_step": kms / ms if ms else None,
+                "compulsory_bytes_per_launch": comp * args.steps / max(kn, 1),
+                "frac_compulsory": (comp * args.steps / max(kn, 1)) / (avg_ms / 1e3) / 1e9 / peak if kn else None,
+                "note": "achieved = untiled-chain (algorithmic) bytes / kernel time; >1 means on-chip reuse. "
+                        "frac_compulsory uses the bytes a fully fused chain must move."}
+
+    # ---- untiled executor on the same inputs (tiled-vs-untiled speedup) -------
+    untiled_value = None
+    if tiled and not args.no_untiled:
+        del rt, cfg, step
+        rtu, cfgu, stepu = build(parse_mode("untiled"))
+        for _ in range(args.warmup):
+            stepu()
+        msu = time_steps(rtu, stepu, args.steps)
+        untiled_value = cu * args.steps * world / (max_over_ranks(msu, dist) / 1e3)
+        del rtu, cfgu, stepu
+
+    # ---- end-to-end through the public API with host buffers --------------------
+    e2e = None
+    if not args.no_e2e:
+        rte, cfge, stepe = build(mode)
+        ids = list(cfge.init.keys())
+        host = {}
+        for ds in ids:
+            t = torch.empty(cfge.init[ds].shape, dtype=torch.float64, pin_memory=True)
+            t.numpy()[...] = cfge.init[ds]
+            host[ds] = t.numpy()
+        out = {ds: torch.empty(cfge.init[ds].shape, dtype=torch.float64, pin_memory=True).numpy() for ds in ids}
+        for _ in range(args.warmup):
+            stepe()
+        rte.synchronize()
+        barrier(dist)
+        t0 = time.perf_counter()
+        for ds in ids:
+            rte.upload(ds, host[ds])
+        for _ in range(args.steps):
+            stepe()
+        for ds in ids:
+            out[ds][...] = rte.download(ds)
+        rte.synchronize()
+        dt = max_over_ranks(time.perf_counter() - t0, dist)
+        nbytes = sum(host[ds].nbytes for ds in ids)
+        e2e = {"value": cu * args.steps * world / dt, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes / args.steps,
+               "d2h_bytes_per_step": (nbytes + 8 * args.steps * (1 if args.config != "c4" else 2)) / args.steps,
+               "definition": "job = upload all fields (pinned) + K steps (per-step reduction read back) + "
+                             "download all fields; per-step bytes = job bytes / K"}
+        del rte, cfge, stepe
+
+    # ---- CPU baseline (reference library on the host cores) ----------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, err = cpu_reference(args.config, 3, 0, budget_s=args.ref_budget / 2)
+        if cpu is None:
+            cpu = {"value": None, "unavailable": err}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic: seeded PCG64 fields with the BASELINE config shapes and value ranges",
+                "config": {"workload": WORKLOAD_TEXT[args.config], "mode": args.mode,
+                           "parallelism": "replicas" if world > 1 else "single GPU",
+                           "l2": "inputs exceed the 126 MB L2; no flush needed",
+                           "effective_GBps": alg * args.steps * world / (ms / 1e3) / 1e9,
+                           "untiled_value": untiled_value,
+                           "speedup_vs_untiled": value / untiled_value if untiled_value else None,
+                           "plan": {k: report.get(k) for k in ("tile_sizes", "cta_grid", "ctas", "max_skew",
+                                                                "subchains", "computed_points")}},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

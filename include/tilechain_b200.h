@@ -115,12 +115,22 @@ int tcg_gpu_plan_pending(tcg_runtime* rt, int mode, const int64_t tile_sizes[3],
 int tcg_signature_pending(tcg_runtime* rt, uint64_t* out);
 int tcg_auto_tile_size(int dim, int64_t cache_bytes, int32_t threads, int64_t bytes_per_point,
                        const int64_t extent[6], int64_t out[3]);
+/* Selects the CUDA device for runtimes created afterwards on this thread
+ * (one process per GPU: pass LOCAL_RANK). */
+int tcg_select_device(int device);
 /* Name, SM count, shared memory, L2 of the executor device (initialises CUDA). */
 int tcg_device_info(char* name, size_t n, int32_t* num_sms, int64_t* smem_optin, int64_t* l2_bytes);
 /* Launch count and the CUDA stream of a runtime's executor (for timing). */
 int tcg_launches(tcg_runtime* rt, int64_t* out);
 int tcg_stream(tcg_runtime* rt, void** out);
 int tcg_body_known(int32_t body);
+/* Device-time instrumentation of the executor kernels (CUDA events on the
+ * executor stream). tcg_kernel_timing synchronizes, returns the accumulated
+ * milliseconds and launch counts of k_tiled and k_untiled since the last call,
+ * and resets them. */
+int tcg_set_timing(tcg_runtime* rt, int on);
+int tcg_kernel_timing(tcg_runtime* rt, double* tiled_ms, int64_t* tiled_launches, double* untiled_ms,
+                      int64_t* untiled_launches);
 
 #ifdef __cplusplus
 }

@@ -17,8 +17,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
-OBJ_DIR = LIB_DIR / "obj"
-LIB = LIB_DIR / "libtcg.so"
+DEBUG = os.environ.get("TCG_DEBUG_BUILD") == "1"  # device printf diagnostics, separate .so
+OBJ_DIR = LIB_DIR / ("obj_debug" if DEBUG else "obj")
+LIB = LIB_DIR / ("libtcg_debug.so" if DEBUG else "libtcg.so")
 REPO = PKG.parent
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -29,13 +30,17 @@ CXXFLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra
 NVCCFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler", "-fPIC",
                     "--expt-relaxed-constexpr", "-Xptxas", "-v", f"-I{REPO / 'include'}"]
 
+if DEBUG:
+    NVCCFLAGS = NVCCFLAGS + ["-DTCG_DEBUG_PRINT"]
+
 HOST_SRCS = ["host/tcg_plan.cpp", "host/tcg_gpuplan.cpp", "host/tcg_runtime.cpp", "tcg_capi.cpp"]
 CUDA_SRCS = ["cuda/tcg_exec.cu"]
 
 
 def _headers() -> list[Path]:
-    hs = [p for p in CSRC.rglob("*.h*")]
+    hs = [p for p in CSRC.rglob("*") if p.suffix in (".h", ".hpp", ".cuh", ".inl")]
     hs += list((REPO / "include").glob("*.h"))
+    hs.append(Path(__file__))
     return hs
 
 

@@ -117,7 +117,7 @@ struct GAcc {
   __device__ __forceinline__ bool reduces() const { return L.has_red != 0; }
 };
 
-template <int DIM>
+template <int DIM, int BODY>
 __global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch L) {
   int64_t x, y = 0, z = 0;
   bool active;
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch
     active = x < L.lo[0] + L.n[0] && y < L.lo[1] + L.n[1];
   }
   GAcc acc{L, x, y, z, red_identity(L.red_op)};
-  if (active) tcb::run_body(L.body, acc, L.prm);
+  if (active) tcb::run_body(BODY, acc, L.prm);
   if (L.has_red) {
     const double v = block_reduce(acc.acc, L.red_op);
     if (threadIdx.x == 0 && threadIdx.y == 0)
@@ -144,9 +144,22 @@ __global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch
 #include "tcg_tiled.cuh"
 
 
+// Launch of k_tiled<DIM, NT>: NT = 512 / (CTAs per SM) threads.
+template <int DIM, int NT>
+void launch_tiled_nt(const DevTiledPlan& P, int64_t smem, cudaStream_t st) {
+  TCG_CK(cudaFuncSetAttribute(tiled::k_tiled<DIM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem)));
+  tiled::k_tiled<DIM, NT><<<dim3(static_cast<unsigned>(P.nctas)), dim3(NT), smem, st>>>(P);
+}
+
 template <int DIM>
-void set_tiled_smem(int64_t bytes) {
-  TCG_CK(cudaFuncSetAttribute(tiled::k_tiled<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+void launch_tiled(const DevTiledPlan& P, int threads, int64_t smem, cudaStream_t st) {
+  if (threads == 512)
+    launch_tiled_nt<DIM, 512>(P, smem, st);
+  else if (threads == 256)
+    launch_tiled_nt<DIM, 256>(P, smem, st);
+  else
+    launch_tiled_nt<DIM, 128>(P, smem, st);
 }
 
 }  // namespace
@@ -170,6 +183,14 @@ struct DeviceExec::PlanBufs {
   int32_t* wboxes = nullptr;
 };
 
+void select_device(int device) {
+  int ndev = 0;
+  TCG_CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    throw InvalidArgument("select_device: device " + std::to_string(device) + " of " + std::to_string(ndev));
+  TCG_CK(cudaSetDevice(device));
+}
+
 DeviceExec::DeviceExec() {
   int ndev = 0;
   TCG_CK(cudaGetDeviceCount(&ndev));
@@ -179,6 +200,7 @@ DeviceExec::DeviceExec() {
   TCG_CK(cudaGetDeviceProperties(&prop, info_.device));
   info_.num_sms = prop.multiProcessorCount;
   info_.smem_optin = static_cast<int64_t>(prop.sharedMemPerBlockOptin);
+  info_.smem_per_sm = static_cast<int64_t>(prop.sharedMemPerMultiprocessor);
   info_.l2_bytes = prop.l2CacheSize;
   info_.name = prop.name;
   if (prop.major < 10) throw CudaError("executor is built for sm_100a (B200); found " + info_.name);
@@ -311,6 +333,43 @@ void DeviceExec::download_async(int f, double* host) {
 
 void DeviceExec::synchronize() { TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_))); }
 
+void* DeviceExec::take_event() {
+  if (!ev_pool_.empty()) {
+    void* e = ev_pool_.back();
+    ev_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  TCG_CK(cudaEventCreate(&e));
+  return e;
+}
+
+void DeviceExec::set_timing(bool on) {
+  timing_ = on;
+  double a, b;
+  int64_t c, d;
+  kernel_ms(&a, &c, &b, &d);  // drain and reset
+}
+
+void DeviceExec::kernel_ms(double* tiled_ms, int64_t* tiled_n, double* untiled_ms, int64_t* untiled_n) {
+  TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+  auto drain = [&](std::vector<std::pair<void*, void*>>& v, double* ms, int64_t* n) {
+    double acc = 0;
+    for (auto& p : v) {
+      float f = 0;
+      TCG_CK(cudaEventElapsedTime(&f, static_cast<cudaEvent_t>(p.first), static_cast<cudaEvent_t>(p.second)));
+      acc += f;
+      ev_pool_.push_back(p.first);
+      ev_pool_.push_back(p.second);
+    }
+    *ms = acc;
+    *n = static_cast<int64_t>(v.size());
+    v.clear();
+  };
+  drain(ev_tiled_, tiled_ms, tiled_n);
+  drain(ev_untiled_, untiled_ms, untiled_n);
+}
+
 void* DeviceExec::ensure_scratch(size_t bytes) {
   if (bytes > scratch_bytes_) {
     if (scratch_) {
@@ -335,11 +394,15 @@ double* DeviceExec::ensure_partials(size_t n) {
   return partials_;
 }
 
-int64_t DeviceExec::window_budget_doubles(int nloops, int nred) const {
-  const int64_t fixed = static_cast<int64_t>(sizeof(tiled::Shared)) + 512 + 256 + static_cast<int64_t>(nloops) * kMaxArgs * 16;
-  const int64_t bytes = info_.smem_optin - fixed - static_cast<int64_t>(nloops) * static_cast<int64_t>(sizeof(DevLoop)) -
-                        static_cast<int64_t>(nred) * kTiledThreads * 8;
-  return std::max<int64_t>(0, bytes / 8);
+int64_t DeviceExec::window_budget_doubles(int nloops, int nred, int ctas_per_sm) const {
+  const int k = std::max(1, ctas_per_sm);
+  const int threads = kTiledThreads / k;
+  // Per-CTA share of the SM (1 KB of every CTA's share is reserved by the driver).
+  const int64_t per_block = std::min<int64_t>(info_.smem_optin, info_.smem_per_sm / k - 1024);
+  const int64_t fixed = static_cast<int64_t>(sizeof(tiled::Shared)) + 512 + 256 +
+                        static_cast<int64_t>(nloops) * (kMaxArgs * 16 + 6 * 4 + static_cast<int64_t>(sizeof(DevLoop))) +
+                        static_cast<int64_t>(nred) * threads * 8;
+  return std::max<int64_t>(0, (per_block - fixed) / 8);
 }
 
 namespace {
@@ -435,13 +498,29 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
       }
       continue;
     }
-    if (ch.dim == 1)
-      k_untiled<1><<<grid, block, 0, st>>>(L);
-    else if (ch.dim == 2)
-      k_untiled<2><<<grid, block, 0, st>>>(L);
-    else
-      k_untiled<3><<<grid, block, 0, st>>>(L);
+    void* e0 = nullptr;
+    if (timing_) {
+      e0 = take_event();
+      TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e0), st));
+    }
+    // One kernel instantiation per (dim, body): the body is a compile-time
+    // constant inside the kernel.
+    const bool known = tcb::dispatch(L.body, [&](auto tag) {
+      constexpr int B = decltype(tag)::value;
+      if (ch.dim == 1)
+        k_untiled<1, B><<<grid, block, 0, st>>>(L);
+      else if (ch.dim == 2)
+        k_untiled<2, B><<<grid, block, 0, st>>>(L);
+      else
+        k_untiled<3, B><<<grid, block, 0, st>>>(L);
+    });
+    if (!known) throw InvalidArgument("untiled executor: body " + std::to_string(L.body) + " not in the registry");
     TCG_CK(cudaGetLastError());
+    if (timing_) {
+      void* e1 = take_event();
+      TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e1), st));
+      ev_untiled_.emplace_back(e0, e1);
+    }
     ++launches_;
     if (L.has_red) {
       k_fold<<<1, 1024, 0, st>>>(L.partials, nblocks, L.red_op, red_dev_ + lp.red);
@@ -497,6 +576,7 @@ void DeviceExec::run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t 
   P.nred = gp.nred;
   P.nctas = static_cast<int32_t>(gp.ctas.size());
   P.smem_doubles = static_cast<int32_t>((gp.smem_doubles + 1) / 2 * 2);
+  P.prefetch = gp.prefetch ? 1 : 0;
   P.ctas = pb->ctas;
   P.boxes = pb->boxes;
   P.win = pb->win;
@@ -513,21 +593,27 @@ void DeviceExec::run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t 
   for (int r = 0; r < gp.nred && r < kMaxRed; ++r) P.red_op[r] = ch.red_op[static_cast<size_t>(r)];
   if (gp.nred > 0) P.red_partials = ensure_partials(static_cast<size_t>(gp.nred) * gp.ctas.size());
   P.red_out = red_dev_;
-  const int64_t smem = static_cast<int64_t>(P.smem_doubles) * 8 + static_cast<int64_t>(gp.nloops) * (sizeof(DevLoop) + kMaxArgs * 16) +
-                       static_cast<int64_t>(gp.nred) * kTiledThreads * 8;
+  const int64_t smem = static_cast<int64_t>(P.smem_doubles) * 8 +
+                       static_cast<int64_t>(gp.nloops) * (sizeof(DevLoop) + kMaxArgs * 16 + 6 * 4) +
+                       static_cast<int64_t>(gp.nred) * gp.threads * 8;
   if (smem > info_.smem_optin) throw PlanError("tiled executor: shared memory request exceeds the device limit");
-  const dim3 grid(static_cast<unsigned>(gp.ctas.size())), block(kTiledThreads);
-  if (gp.dim == 1) {
-    set_tiled_smem<1>(smem);
-    tiled::k_tiled<1><<<grid, block, smem, st>>>(P);
-  } else if (gp.dim == 2) {
-    set_tiled_smem<2>(smem);
-    tiled::k_tiled<2><<<grid, block, smem, st>>>(P);
-  } else {
-    set_tiled_smem<3>(smem);
-    tiled::k_tiled<3><<<grid, block, smem, st>>>(P);
+  void* e0 = nullptr;
+  if (timing_) {
+    e0 = take_event();
+    TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e0), st));
   }
+  if (gp.dim == 1)
+    launch_tiled<1>(P, gp.threads, smem, st);
+  else if (gp.dim == 2)
+    launch_tiled<2>(P, gp.threads, smem, st);
+  else
+    launch_tiled<3>(P, gp.threads, smem, st);
   TCG_CK(cudaGetLastError());
+  if (timing_) {
+    void* e1 = take_event();
+    TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e1), st));
+    ev_tiled_.emplace_back(e0, e1);
+  }
   ++launches_;
   for (int k = 0; k < gp.ndat; ++k)
     if (gp.dats[static_cast<size_t>(k)].pingpong) swap(gp.dat_ids[static_cast<size_t>(k)]);

@@ -71,7 +71,8 @@ struct DevDat {
   int32_t pingpong;   // src != dst: read old, write owned points to the other buffer
   int32_t wbox_off;   // in-place write-back boxes: wboxes[(wbox_off + i)*6 ..]
   int32_t nwbox;
-  int32_t pad;
+  int32_t reach;      // R: largest |stream offset| of any read; windows keep R
+                      // mirror rows on each side so reads never wrap
 };
 
 struct DevTiledPlan {
@@ -81,6 +82,7 @@ struct DevTiledPlan {
   int32_t nred;
   int32_t nctas;
   int32_t smem_doubles;  // max over CTAs (window storage only)
+  int32_t prefetch;      // windows are deep enough to load slab t+1 while slab t computes
   const DevCta* ctas;
   const int32_t* boxes;
   const int32_t* win;

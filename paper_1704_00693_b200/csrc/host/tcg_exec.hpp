@@ -27,6 +27,7 @@ struct DeviceInfo {
   int device = 0;
   int num_sms = 0;
   int64_t smem_optin = 0;
+  int64_t smem_per_sm = 0;
   int64_t l2_bytes = 0;
   std::string name;
 };
@@ -36,6 +37,9 @@ struct ExecTiming {
   int launches = 0;
   double gpu_ms = 0;
 };
+
+// cudaSetDevice in this library's CUDA runtime (one process per GPU).
+void select_device(int device);
 
 class DeviceExec {
  public:
@@ -69,8 +73,13 @@ class DeviceExec {
   void synchronize();
   void* stream() const { return stream_; }
   int64_t launches() const { return launches_; }
+  // Kernel timing: when enabled, CUDA events bracket every main executor
+  // kernel (k_tiled, k_untiled) on the executor stream; kernel_ms() syncs and
+  // returns the accumulated device time and launch count since the last reset.
+  void set_timing(bool on);
+  void kernel_ms(double* tiled_ms, int64_t* tiled_n, double* untiled_ms, int64_t* untiled_n);
   // Bytes of dynamic shared memory available for windows for a chain shape.
-  int64_t window_budget_doubles(int nloops, int nred) const;
+  int64_t window_budget_doubles(int nloops, int nred, int ctas_per_sm) const;
 
  private:
   struct Buf;
@@ -86,6 +95,10 @@ class DeviceExec {
   double* red_dev_ = nullptr;
   std::vector<std::pair<uint64_t, PlanBufs*>> plan_cache_;
   int64_t launches_ = 0;
+  bool timing_ = false;
+  std::vector<std::pair<void*, void*>> ev_tiled_, ev_untiled_;  // (start, stop) event pairs
+  std::vector<void*> ev_pool_;
+  void* take_event();
   void* ensure_scratch(size_t bytes);
   double* ensure_partials(size_t n);
   PlanBufs* plan_bufs(const GpuTiledPlan& gp, uint64_t key);

@@ -16,6 +16,7 @@ int64_t ceil_even(int64_t v) { return floor_even(v + 1); }
 struct DatInfo {
   DatasetId id;
   bool load = false, written = false, pingpong = false;
+  int64_t reach = 0;  // max |stream-dim offset| of reads (mirror rows per side)
   std::vector<Range> wboxes;
 };
 
@@ -46,6 +47,12 @@ std::vector<DatInfo> classify(const LoopChain& chain, std::vector<int>& slot_of)
   for (const LoopRecord& lp : chain.loops) {
     for (const ArgSpec& a : lp.args) {
       DatInfo& di = out[static_cast<size_t>(slot(a.dataset))];
+      if (mode_reads(a.mode)) {
+        const Stencil& st = chain.stencil(a.stencil);
+        const int s = chain.dim - 1;
+        di.reach = std::max({di.reach, static_cast<int64_t>(std::llabs(st.min_offset(s))),
+                             static_cast<int64_t>(std::llabs(st.max_offset(s)))});
+      }
       if (!mode_reads(a.mode) || di.load) continue;
       const Stencil& st = chain.stencil(a.stencil);
       Range rb = lp.range;
@@ -71,26 +78,55 @@ struct Layout {
   RankLayout ranks;
   std::array<int64_t, kMaxDims> block{0, 0, 0};
   int64_t stream_tile = 1;
+  bool prefetch = false;
 };
 
+int64_t floor_div(int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// CTA decomposition of the union bounds. Column dims are cut at multiples of
+// an even block width in ABSOLUTE coordinates, so interior ownership
+// boundaries are 16-byte aligned in every dataset (bulk-copy evictions); the
+// stream dim is split into near-equal segments like the reference's
+// decompose (dist.cpp:142-177). Ranks are lexicographic, dim 0 slowest.
 Layout make_layout(const Range& U, int dim, const std::array<int64_t, kMaxDims>& block, int64_t stile, int nseg) {
   Layout L;
   const int s = dim - 1;
-  std::array<int, kMaxDims> g{1, 1, 1};
-  for (int d = 0; d < dim; ++d) {
-    const int64_t ext = std::max<int64_t>(1, U.extent(d));
-    if (d == s) {
-      g[d] = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nseg, ext)));
-    } else {
-      const int64_t b = std::max<int64_t>(1, block[d]);
-      g[d] = static_cast<int>(std::min<int64_t>(ext, (ext + b - 1) / b));
-    }
-  }
-  // An empty union (all loops empty) still needs one CTA.
-  Range Ug = U;
+  Range Ug = U;  // an empty union (all loops empty) still needs one CTA
   for (int d = 0; d < dim; ++d)
     if (Ug.extent(d) <= 0) Ug.set(d, U.start(d), U.start(d) + 1);
-  L.ranks = decompose(Ug, g);
+  std::array<std::vector<int64_t>, kMaxDims> cuts;
+  for (int d = 0; d < dim; ++d) {
+    const int64_t lo = Ug.start(d), hi = Ug.end(d), ext = hi - lo;
+    std::vector<int64_t>& c = cuts[d];
+    c.push_back(lo);
+    if (d == s) {
+      const int64_t g = std::max<int64_t>(1, std::min<int64_t>(nseg, ext));
+      const int64_t q = ext / g, rem = ext % g;
+      int64_t p = lo;
+      for (int64_t i = 0; i < g; ++i) {
+        p += q + (i < rem ? 1 : 0);
+        c.push_back(p);
+      }
+    } else {
+      int64_t b = std::max<int64_t>(2, block[d]);
+      b += b & 1;
+      for (int64_t p = floor_div(lo, b) * b + b; p < hi; p += b) c.push_back(p);
+      c.push_back(hi);
+    }
+  }
+  RankLayout& R = L.ranks;
+  R.dim = dim;
+  R.global = Ug;
+  for (int d = 0; d < kMaxDims; ++d) R.grid[d] = d < dim ? static_cast<int>(cuts[d].size()) - 1 : 1;
+  const int total = R.grid[0] * R.grid[1] * R.grid[2];
+  R.owned.assign(static_cast<size_t>(total), Range(dim));
+  for (int r = 0; r < total; ++r) {
+    const auto co = R.coords_of(r);
+    Range own(dim);
+    for (int d = 0; d < dim; ++d)
+      own.set(d, cuts[d][static_cast<size_t>(co[d])], cuts[d][static_cast<size_t>(co[d]) + 1]);
+    R.owned[static_cast<size_t>(r)] = own;
+  }
   L.block = block;
   L.stream_tile = std::max<int64_t>(1, stile);
   return L;
@@ -188,15 +224,13 @@ CtaBuild build_cta(const LoopChain& chain, const std::vector<DatInfo>& dats, con
         }
       }
     }
-  // Window columns: every access, plus the write-back columns when some
-  // dataset is ping-ponged (its second buffer must be completed by the owner).
-  for (int d = 0; d < s; ++d) {
-    if (any_pp) {
-      col_lo[d] = std::min<int64_t>(col_lo[d], c.wb_lo[d]);
-      col_hi[d] = std::max<int64_t>(col_hi[d], c.wb_hi[d]);
-    }
+  // Window columns: every access of this CTA's plan. Write-back points of a
+  // ping-ponged dataset outside the window are never written by the chain
+  // (they lie outside the union bounds), so the kernel copies them
+  // global-to-global instead of staging them.
+  (void)any_pp;
+  for (int d = 0; d < s; ++d)
     if (col_lo[d] > col_hi[d]) col_lo[d] = col_hi[d] = own.start(d);
-  }
   if (s >= 1) {
     col_lo[0] = floor_even(col_lo[0]);
     col_hi[0] = ceil_even(col_hi[0]);
@@ -239,8 +273,11 @@ CtaBuild build_cta(const LoopChain& chain, const std::vector<DatInfo>& dats, con
       lo[static_cast<size_t>(t)] = std::min(lo[static_cast<size_t>(t)], hi[static_cast<size_t>(t) - 1]);
     for (int64_t t = 0; t < T; ++t) lo[static_cast<size_t>(t)] = std::min(lo[static_cast<size_t>(t)], hi[static_cast<size_t>(t)]);
     lo[static_cast<size_t>(T)] = hi[static_cast<size_t>(T) - 1];
+    // Depth covers the rows of slab t, plus (prefetch) those loaded for slab
+    // t+1 while t computes: rows [lo(t), hi(t+1)).
     int64_t W = 0;
-    for (int64_t t = 0; t < T; ++t) W = std::max(W, hi[static_cast<size_t>(t)] - lo[static_cast<size_t>(t)]);
+    for (int64_t t = 0; t < T; ++t)
+      W = std::max(W, hi[static_cast<size_t>(lay.prefetch ? std::min(t + 1, T - 1) : t)] - lo[static_cast<size_t>(t)]);
     W = std::max<int64_t>(W, 1);
     for (int64_t t = 0; t <= T; ++t) {
       int32_t* w = &cb.win[(static_cast<size_t>(t) * nd + k) * 2];
@@ -259,12 +296,13 @@ struct Candidate {
   std::array<int64_t, kMaxDims> block{0, 0, 0};
   int64_t stile = 1;
   int nseg = 1;
+  int k = 1;  // CTAs per SM
 };
 
 }  // namespace
 
 GpuTiledPlan build_gpu_tiled_plan(const LoopChain& chain, const std::vector<FieldGeom>& fields,
-                                  const GpuTileChoice& choice, int64_t budget, int num_sms) {
+                                  const GpuTileChoice& choice, const WindowBudget& budget_fn, int num_sms) {
   const auto t0 = std::chrono::steady_clock::now();
   if (chain.empty()) throw PlanError("build_gpu_tiled_plan: empty chain");
   const int dim = chain.dim, s = dim - 1;
@@ -314,6 +352,9 @@ GpuTiledPlan build_gpu_tiled_plan(const LoopChain& chain, const std::vector<Fiel
       by_list = pick(choice.block[1], {32, 16, 8, 4});
       st_list = pick(choice.stream_tile, {4, 2, 1});
     }
+    const std::vector<int> k_list = choice.ctas_per_sm > 0 ? std::vector<int>{choice.ctas_per_sm}
+                                                           : std::vector<int>{2, 1, 4};
+    for (int k : k_list)
     for (int64_t st : st_list)
       for (int64_t bx : bx_list)
         for (int64_t by : by_list) {
@@ -321,15 +362,30 @@ GpuTiledPlan build_gpu_tiled_plan(const LoopChain& chain, const std::vector<Fiel
           if (dim >= 2) c.block[0] = bx;
           if (dim == 3) c.block[1] = by;
           c.stile = st;
+          c.k = k;
+          const int64_t slots = static_cast<int64_t>(num_sms) * k;
           // Stream segments: fill the SMs when the column grid alone cannot.
           int64_t cols = 1;
           for (int d = 0; d < s; ++d) cols *= (std::max<int64_t>(1, U.extent(d)) + c.block[d] - 1) / c.block[d];
           if (choice.stream_segments > 0) {
             c.nseg = choice.stream_segments;
           } else {
-            const int64_t want = std::max<int64_t>(1, (num_sms + cols - 1) / cols);
-            const int64_t max_seg = std::max<int64_t>(1, U.extent(s) / 64);
-            c.nseg = static_cast<int>(std::min(want, max_seg));
+            // Wave-aware: one CTA per SM, so the critical path is
+            // waves * (rows per segment + per-segment warm-up skew).
+            const int64_t ext = std::max<int64_t>(1, U.extent(s));
+            const int64_t max_seg = std::max<int64_t>(1, ext / 32);
+            const int64_t warm = 2 * st + 8;
+            int64_t best = 1;
+            double best_cost = 1e300;
+            for (int64_t g = 1; g <= max_seg; ++g) {
+              const int64_t waves = (cols * g + slots - 1) / slots;
+              const double cost = static_cast<double>(waves) * (static_cast<double>(ext) / g + warm);
+              if (cost < best_cost * 0.999) {
+                best_cost = cost;
+                best = g;
+              }
+            }
+            c.nseg = static_cast<int>(best);
           }
           cands.push_back(c);
         }
@@ -337,7 +393,9 @@ GpuTiledPlan build_gpu_tiled_plan(const LoopChain& chain, const std::vector<Fiel
 
   std::string last_err = "no candidate";
   for (const Candidate& cand : cands) {
-    const Layout lay = make_layout(U, dim, cand.block, cand.stile, cand.nseg);
+    Layout lay = make_layout(U, dim, cand.block, cand.stile, cand.nseg);
+    lay.prefetch = choice.prefetch != 0;
+    const int64_t budget = budget_fn(cand.k);
     // Cheap probe with the middle CTA before building all of them.
     const int probe = lay.ranks.rank_count() / 2;
     if (build_cta(chain, dats, slot_of, fields, lay, probe).smem > budget) {
@@ -360,6 +418,9 @@ GpuTiledPlan build_gpu_tiled_plan(const LoopChain& chain, const std::vector<Fiel
     gp.grid = lay.ranks.grid;
     gp.block = cand.block;
     gp.stream_tile = cand.stile;
+    gp.prefetch = lay.prefetch;
+    gp.ctas_per_sm = cand.k;
+    gp.threads = 512 / cand.k;
     for (CtaBuild& cb : builds) {
       cb.cta.box_off = static_cast<int32_t>(gp.boxes.size());
       cb.cta.win_off = static_cast<int32_t>(gp.win.size());
@@ -378,6 +439,7 @@ GpuTiledPlan build_gpu_tiled_plan(const LoopChain& chain, const std::vector<Fiel
       dd.pingpong = di.pingpong;
       dd.wbox_off = static_cast<int32_t>(gp.wboxes.size() / 6);
       dd.nwbox = di.pingpong ? 0 : static_cast<int32_t>(di.wboxes.size());
+      dd.reach = static_cast<int32_t>(di.reach);
       if (!di.pingpong)
         for (const Range& r : di.wboxes)
           for (int d = 0; d < 3; ++d) {

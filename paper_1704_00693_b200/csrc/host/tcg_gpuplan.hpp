@@ -24,7 +24,13 @@ struct GpuTileChoice {
   std::array<int64_t, kMaxDims> block{0, 0, 0};  // owned CTA extent per non-stream dim (0 = auto)
   int64_t stream_tile = 0;                        // skewed slab height along the stream dim (0 = auto)
   int stream_segments = 0;                        // CTA segments along the stream dim (0 = auto)
+  int prefetch = 0;                               // 1: deepen windows to overlap slab loads with compute
+  int ctas_per_sm = 0;                            // 1, 2 or 4 resident CTAs per SM (0 = auto)
 };
+
+// Window storage (doubles) available to one CTA when `ctas_per_sm` CTAs of
+// 512 / ctas_per_sm threads share an SM.
+using WindowBudget = std::function<int64_t(int ctas_per_sm)>;
 
 struct GpuTiledPlan {
   int dim = 1;
@@ -39,6 +45,9 @@ struct GpuTiledPlan {
   std::array<int, kMaxDims> grid{1, 1, 1};
   std::array<int64_t, kMaxDims> block{0, 0, 0};
   int64_t stream_tile = 1;
+  bool prefetch = false;
+  int ctas_per_sm = 1;
+  int threads = 512;
   std::array<int64_t, kMaxDims> max_skew{0, 0, 0};
   // Accounting: points computed (incl. redundant) vs recorded.
   int64_t computed_points = 0;
@@ -46,9 +55,9 @@ struct GpuTiledPlan {
   double build_seconds = 0;
 };
 
-// smem_budget_doubles: per-CTA window budget. Throws PlanError if the
-// explicit choice does not fit; auto fields are searched.
+// budget(k): per-CTA window storage with k CTAs per SM. Throws PlanError
+// ("no CTA tiling fits") when nothing fits; auto fields are searched.
 GpuTiledPlan build_gpu_tiled_plan(const LoopChain& chain, const std::vector<FieldGeom>& fields,
-                                  const GpuTileChoice& choice, int64_t smem_budget_doubles, int num_sms);
+                                  const GpuTileChoice& choice, const WindowBudget& budget, int num_sms);
 
 }  // namespace tcg

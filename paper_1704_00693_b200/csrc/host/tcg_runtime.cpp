@@ -271,6 +271,8 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
     }
   }
   choice.stream_segments = cfg_.stream_segments;
+  if (const char* e = std::getenv("TCG_PREFETCH")) choice.prefetch = std::atoi(e);
+  if (const char* e = std::getenv("TCG_CTAS_PER_SM")) choice.ctas_per_sm = std::atoi(e);
   const std::vector<FieldGeom> geoms = field_geoms();
   const uint64_t sig = chain.signature();
   rep.plan_cache_hit = true;
@@ -290,7 +292,8 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
     for (const auto& l : sub.loops) nred += l.reduction ? 1 : 0;
     std::shared_ptr<const GpuTiledPlan> gp;
     try {
-      const int64_t budget = dev.window_budget_doubles(static_cast<int>(sub.size()), nred);
+      const int nl = static_cast<int>(sub.size());
+      const WindowBudget budget = [&](int k) { return dev.window_budget_doubles(nl, nred, k); };
       auto p = std::make_shared<GpuTiledPlan>(build_gpu_tiled_plan(sub, geoms, choice, budget, dev.info().num_sms));
       ++gpu_plan_builds_;
       ++rep.plan_constructions;

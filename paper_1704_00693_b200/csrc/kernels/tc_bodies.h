@@ -190,6 +190,37 @@ TC_HD bool body_known(int32_t b) {
   }
 }
 
+// Compile-time body list for executors that hoist the dispatch out of the
+// per-point loop (one specialised point loop per body).
+#define TCB_CORE_BODIES(X)                                                                              \
+  X(kGenSum) X(kJacobiStencil) X(kJacobiCopy) X(kMhEos) X(kMhBcX) X(kMhBcY) X(kMhAccelX) X(kMhAccelY)    \
+  X(kMhFluxX) X(kMhFluxY) X(kMhAdvectRho) X(kMhAdvectE) X(kMhSmooth) X(kMhBlend) X(kMhMonitor)          \
+  X(kSmooth2D) X(kSmooth1D) X(kConsume1D) X(kCopy) X(kSumRead) X(kIota) X(kNbrSum) X(kHeatLap)         \
+  X(kHeatCopy) X(kHydroBase + 0) X(kHydroBase + 1) X(kHydroBase + 2) X(kHydroBase + 3)                 \
+  X(kHydroBase + 4) X(kHydroBase + 5) X(kHydroBase + 6) X(kHydroBase + 7) X(kHydroBase + 8)             \
+  X(kHydroBase + 9) X(kHydroCfl) X(kJacobi3D) X(kCgPUpdate) X(kCgMatvec) X(kCgXUpdate) X(kCgRUpdate)    \
+  X(kCgDot)
+
+template <int B>
+struct BodyTag {
+  static constexpr int value = B;
+};
+
+// Calls f(BodyTag<body>{}) for a registered body; false if unknown.
+template <class F>
+TC_HD bool dispatch(int32_t body, F&& f) {
+  switch (body) {
+#define TCB_CASE(B) \
+  case B:           \
+    f(BodyTag<B>{}); \
+    return true;
+    TCB_CORE_BODIES(TCB_CASE)
+#undef TCB_CASE
+    default:
+      return ns_dispatch(body, f);
+  }
+}
+
 // Dispatch one body at one point. Returns false for an unknown id.
 template <class A>
 TC_HD bool run_body(int32_t body, A& a, const double* p) {

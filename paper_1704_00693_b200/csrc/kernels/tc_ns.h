@@ -12,4 +12,9 @@ TC_HD bool ns_run_body(int32_t, A&, const double*) {
   return false;
 }
 
+template <class F>
+TC_HD bool ns_dispatch(int32_t, F&&) {
+  return false;
+}
+
 }  // namespace tcb

@@ -257,9 +257,14 @@ int tcg_gpu_plan_pending(tcg_runtime* rt, int mode, const int64_t ts[3], char* b
     choice.stream_segments = rt->rt->config().stream_segments;
     int nred = 0;
     for (const auto& l : c.loops) nred += l.reduction ? 1 : 0;
-    const int64_t fixed = 2048 + static_cast<int64_t>(c.size()) * static_cast<int64_t>(sizeof(tcg::DevLoop)) +
-                          static_cast<int64_t>(nred) * 512 * 8;
-    const int64_t budget = (kB200SmemOptin - fixed) / 8;
+    const int nl = static_cast<int>(c.size());
+    const tcg::WindowBudget budget = [&](int k) {
+      const int64_t per_block = std::min<int64_t>(kB200SmemOptin, 233472 / k - 1024);
+      const int64_t fixed = 6144 + nl * (static_cast<int64_t>(sizeof(tcg::DevLoop)) + 12 * 16 + 24) +
+                            static_cast<int64_t>(nred) * (512 / k) * 8;
+      return (per_block - fixed) / 8;
+    };
+    if (const char* e = std::getenv("TCG_CTAS_PER_SM")) choice.ctas_per_sm = std::atoi(e);
     const tcg::GpuTiledPlan gp = tcg::build_gpu_tiled_plan(c, rt->rt->field_geoms(), choice, budget, kB200Sms);
     std::ostringstream os;
     os << "grid=" << gp.grid[0] << "," << gp.grid[1] << "," << gp.grid[2] << " block=" << gp.block[0] << ","
@@ -338,5 +343,17 @@ int tcg_stream(tcg_runtime* rt, void** out) {
 }
 
 int tcg_body_known(int32_t body) { return tcb::body_known(body) ? 1 : 0; }
+
+int tcg_select_device(int device) {
+  return guard([&] { tcg::select_device(device); });
+}
+
+int tcg_set_timing(tcg_runtime* rt, int on) {
+  return guard([&] { rt->rt->device().set_timing(on != 0); });
+}
+
+int tcg_kernel_timing(tcg_runtime* rt, double* tiled_ms, int64_t* tiled_n, double* untiled_ms, int64_t* untiled_n) {
+  return guard([&] { rt->rt->device().kernel_ms(tiled_ms, tiled_n, untiled_ms, untiled_n); });
+}
 
 }  // extern "C"

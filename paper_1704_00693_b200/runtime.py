@@ -25,7 +25,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_lib" / "libtcg.so"
+LIB_PATH = _PKG / "_lib" / ("libtcg_debug.so" if __import__("os").environ.get("TCG_DEBUG_LIB") == "1" else "libtcg.so")
 _lib: Optional[ctypes.CDLL] = None
 
 
@@ -108,6 +108,10 @@ def load_library() -> ctypes.CDLL:
         "tcg_launches": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
         "tcg_stream": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
         "tcg_body_known": (ctypes.c_int, [_I32]),
+        "tcg_set_timing": (ctypes.c_int, [_P, ctypes.c_int]),
+        "tcg_select_device": (ctypes.c_int, [ctypes.c_int]),
+        "tcg_kernel_timing": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64), ctypes.POINTER(_D),
+                                             ctypes.POINTER(_I64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -403,6 +407,17 @@ class Runtime:
         _check(self._lib.tcg_stream(self._h, ctypes.byref(out)))
         return out.value or 0
 
+    def set_timing(self, on: bool = True) -> None:
+        _check(self._lib.tcg_set_timing(self._h, int(on)))
+
+    def kernel_timing(self) -> dict:
+        """Device ms and launch counts of k_tiled / k_untiled since the last call."""
+        tm, tn, um, un = _D(), _I64(), _D(), _I64()
+        _check(self._lib.tcg_kernel_timing(self._h, ctypes.byref(tm), ctypes.byref(tn), ctypes.byref(um),
+                                           ctypes.byref(un)))
+        return {"tiled_ms": tm.value, "tiled_launches": tn.value, "untiled_ms": um.value,
+                "untiled_launches": un.value}
+
 
 def auto_tile_size(dim, cache_bytes, threads, bytes_per_point, extent: Range):
     lib = load_library()
@@ -417,6 +432,11 @@ def device_info() -> dict:
     sms, smem, l2 = _I32(), _I64(), _I64()
     _check(lib.tcg_device_info(name, 256, ctypes.byref(sms), ctypes.byref(smem), ctypes.byref(l2)))
     return {"name": name.value.decode(), "num_sms": sms.value, "smem_optin": smem.value, "l2_bytes": l2.value}
+
+
+def select_device(device: int) -> None:
+    """cudaSetDevice inside libtcg (its CUDA runtime is not torch's)."""
+    _check(load_library().tcg_select_device(device))
 
 
 def body_known(body: int) -> bool:
