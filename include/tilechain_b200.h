@@ -22,6 +22,10 @@
  *   tcg_rank_plans_pending construct_rank_plan + compute_halo_depths          dist.cpp:191-448
  *   tcg_auto_tile_size     auto_tile_size                           tile_sizer.cpp:27-81
  *   tcg_report_text        ExecutionReport::to_text                 executor.cpp:321-366
+ *   tcg_set_rank_grid      Runtime::set_rank_grid (ranks simulated in one process)  runtime.hpp:77-81, runtime.cpp:213-222
+ *   tcg_set_process_rank   one rank per process (DistContext's ranks as processes, NCCL transport)  dist.hpp:96-156
+ *   tcg_dist_schedule_pending  construct_rank_plan + compute_halo_depths + exchange_halos message list
+ *                          for the pending chain (host only)        dist.cpp:191-511
  *
  * Kernels: the reference's KernelHandle{id, name, std::function} becomes
  * (kernel_id, body, params): `body` selects a per-point body compiled into the
@@ -113,6 +117,22 @@ int tcg_rank_plans_pending(tcg_runtime* rt, const int32_t grid[3], const int64_t
 int tcg_gpu_plan_pending(tcg_runtime* rt, int mode, const int64_t tile_sizes[3], char* buf, int64_t n,
                          int64_t* needed);
 int tcg_signature_pending(tcg_runtime* rt, uint64_t* out);
+
+/* Distribution. grid: ranks per dimension (slabs: {1,P,1}
+ * in 2D, {1,1,P} in 3D). tcg_set_rank_grid hosts every rank in this process
+ * on the current GPU; tcg_set_process_rank hosts rank `rank` here and reaches
+ * the others through NCCL: rank 0 calls tcg_comm_unique_id and shares the 128
+ * bytes with every process (e.g. torch.distributed broadcast) before all call
+ * tcg_set_process_rank. Data already uploaded is carried into the rank fields.
+ * In a multi-process job, get() is collective (every process calls it) and
+ * download() fills the regions this process's rank holds. */
+int tcg_set_rank_grid(tcg_runtime* rt, const int32_t grid[3]);
+int tcg_comm_unique_id(uint8_t out[128]);
+/* Owned box of a rank (decompose, dist.cpp:142-177, over the fields' hull). */
+int tcg_rank_owned(tcg_runtime* rt, int32_t rank, int64_t out[6]);
+int tcg_set_process_rank(tcg_runtime* rt, const int32_t grid[3], int32_t rank, const uint8_t id[128]);
+/* Text: "rank=", "loop rank= l= lo hi ...", "msg src= dst= ds= dim= dir= box lo hi ..." lines. */
+int tcg_dist_schedule_pending(tcg_runtime* rt, char* buf, int64_t n, int64_t* needed);
 int tcg_auto_tile_size(int dim, int64_t cache_bytes, int32_t threads, int64_t bytes_per_point,
                        const int64_t extent[6], int64_t out[3]);
 /* Selects the CUDA device for runtimes created afterwards on this thread

@@ -113,6 +113,7 @@ def load_oracle():
             "tco_get_alloc": [_P, ctypes.c_int, _P],
             "tco_par_loop": [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, _P],
             "tco_fetch": [_P, ctypes.c_int, _P],
+            "tco_set_reduction_mask": [_P, _P],
         }.items():
             fn = getattr(lib, n)
             fn.argtypes = a
@@ -314,6 +315,10 @@ class OracleRuntime(_Base):
         out = _D()
         self._ck(self.lib.tco_fetch(self.h, h, ctypes.byref(out)))
         return out.value
+
+    def set_reduction_mask(self, rng):
+        """Only points inside rng contribute to later reductions (None clears)."""
+        self._ck(self.lib.tco_set_reduction_mask(self.h, None if rng is None else _arr(_I64, _lohi(rng))))
 
     def upload(self, ds, data):
         a = np.ascontiguousarray(data, dtype=np.float64)

@@ -58,6 +58,8 @@ struct ORuntime {
   std::vector<OField> fields;
   std::vector<double> reductions;
   std::vector<int> fetched;
+  bool masked = false;            // execute_plan's reduction_mask (executor.cpp:209-250)
+  int64_t mlo[3] = {0, 0, 0}, mhi[3] = {1, 1, 1};
 };
 
 struct OArg {
@@ -71,6 +73,7 @@ struct OAcc {
   int64_t p[3];
   int red_op = -1;
   double* red = nullptr;
+  const ORuntime* rt = nullptr;
 
   [[noreturn]] void fail(const char* why) const { throw std::runtime_error(why); }
   double read(int a, int dx, int dy, int dz) const {
@@ -96,6 +99,9 @@ struct OAcc {
   }
   void contribute(double v) const {
     if (red == nullptr) fail("contribute() without a declared reduction");
+    if (rt && rt->masked)  // kernel_ctx.hpp:87: points outside the mask do not contribute
+      for (int d = 0; d < 3; ++d)
+        if (p[d] < rt->mlo[d] || p[d] >= rt->mhi[d]) return;
     if (red_op == tcb::kSum)
       *red = *red + v;
     else if (red_op == tcb::kMin)
@@ -215,6 +221,7 @@ int64_t tco_par_loop(void* hv, int, int body, int red, const int64_t* range6, in
     acc.args = &a;
     acc.red_op = red;
     acc.red = red >= 0 ? &accum : nullptr;
+    acc.rt = r;
     int64_t lo[3], hi[3];
     for (int d = 0; d < 3; ++d) {
       lo[d] = d < r->dim ? range6[2 * d] : 0;
@@ -233,6 +240,18 @@ int64_t tco_par_loop(void* hv, int, int body, int red, const int64_t* range6, in
     r->fetched.push_back(0);
     return static_cast<int64_t>(r->reductions.size()) - 1;
   });
+}
+
+// Reduction mask for the following loops (NULL clears it); a rank's owned box
+// in the distributed tests.
+int64_t tco_set_reduction_mask(void* hv, const int64_t* range6) {
+  auto* r = static_cast<ORuntime*>(hv);
+  r->masked = range6 != nullptr;
+  for (int d = 0; d < 3; ++d) {
+    r->mlo[d] = range6 && d < r->dim ? range6[2 * d] : 0;
+    r->mhi[d] = range6 && d < r->dim ? range6[2 * d + 1] : 1;
+  }
+  return 0;
 }
 
 int64_t tco_fetch(void* hv, int handle, double* out) {

@@ -7,8 +7,8 @@ sm_100a CUDA executors. See DESIGN.md.
 from . import kernels
 from .runtime import (AccessError, AccessMode, ArgSpec, CudaError, ExecMode, InvalidArgument, KernelHandle,
                       PlanError, Range, ReduceOp, Runtime, RuntimeConfig, SizerError, TcgError, auto_tile_size,
-                      body_known, device_info, load_library, parse_report, LIB_PATH)
+                      body_known, comm_unique_id, device_info, load_library, parse_report, parse_schedule, LIB_PATH)
 
 __all__ = ["kernels", "AccessError", "AccessMode", "ArgSpec", "CudaError", "ExecMode", "InvalidArgument",
            "KernelHandle", "PlanError", "Range", "ReduceOp", "Runtime", "RuntimeConfig", "SizerError", "TcgError",
-           "auto_tile_size", "body_known", "device_info", "load_library", "parse_report", "LIB_PATH"]
+           "auto_tile_size", "body_known", "comm_unique_id", "device_info", "load_library", "parse_report", "parse_schedule", "LIB_PATH"]

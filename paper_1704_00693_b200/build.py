@@ -33,8 +33,8 @@ NVCCFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler
 if DEBUG:
     NVCCFLAGS = NVCCFLAGS + ["-DTCG_DEBUG_PRINT"]
 
-HOST_SRCS = ["host/tcg_plan.cpp", "host/tcg_gpuplan.cpp", "host/tcg_runtime.cpp", "tcg_capi.cpp"]
-CUDA_SRCS = ["cuda/tcg_exec.cu"]
+HOST_SRCS = ["host/tcg_plan.cpp", "host/tcg_gpuplan.cpp", "host/tcg_dist.cpp", "host/tcg_runtime.cpp", "tcg_capi.cpp"]
+CUDA_SRCS = ["cuda/tcg_exec.cu", "cuda/tcg_comm.cu"]
 
 
 def _headers() -> list[Path]:
@@ -81,7 +81,7 @@ def build(verbose: bool = False) -> Path:
             for f in [ex.submit(_compile, c, l) for c, l in jobs]:
                 f.result()
     if jobs or not LIB.exists():
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcuda"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcuda", "-ldl"]
         _compile(cmd, LIB_DIR / "link.log")
     if verbose:
         print(f"built {LIB}")

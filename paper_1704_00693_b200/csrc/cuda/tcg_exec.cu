@@ -84,30 +84,53 @@ struct UArg {
 struct ULaunch {
   int32_t body, nargs, red_op, has_red;
   int64_t lo[3], n[3];
+  int32_t masked, pad_;
+  int64_t mlo[3], mhi[3];  // reduction mask (rank-owned box) when masked
   UArg a[kMaxArgs];
   double prm[kMaxParams];
   DevStencils st;
   double* partials;
 };
 
+// Accessor over HBM. c[a] points at argument a's element for the current
+// point; a thread walks a short run of rows, advancing every pointer by one
+// row pitch. All reads use the read-only (non-coherent) path: legal because
+// a loop never reads a point another point of the same loop writes
+// (runtime.cpp:56-76), and it lets the compiler keep overlapping stencil
+// rows of consecutive points in registers.
 struct GAcc {
   const ULaunch& L;
+  double* c[kMaxArgs];
   int64_t px, py, pz;
   double acc;
   __device__ __forceinline__ double* at(int a, int dx, int dy, int dz) const {
     const UArg& g = L.a[a];
-    return g.base + ((pz + dz - g.z0) * g.pz + (py + dy - g.y0) * g.py + (px + dx - g.x0));
+    return c[a] + (dz * g.pz + dy * g.py + dx);
+  }
+  __device__ __forceinline__ void locate() {
+#pragma unroll
+    for (int a = 0; a < kMaxArgs; ++a) {
+      const UArg& g = L.a[a];
+      c[a] = g.base + ((pz - g.z0) * g.pz + (py - g.y0) * g.py + (px - g.x0));
+    }
+  }
+  template <int DIM>
+  __device__ __forceinline__ void advance() {
+#pragma unroll
+    for (int a = 0; a < kMaxArgs; ++a) c[a] += DIM == 3 ? L.a[a].pz : L.a[a].py;
   }
   __device__ __forceinline__ int64_t x() const { return px; }
   __device__ __forceinline__ int64_t y() const { return py; }
   __device__ __forceinline__ int64_t z() const { return pz; }
-  __device__ __forceinline__ double read(int a, int dx, int dy, int dz) const { return *at(a, dx, dy, dz); }
-  __device__ __forceinline__ void write(int a, double v) const { *at(a, 0, 0, 0) = v; }
-  __device__ __forceinline__ void increment(int a, double v) const {
-    double* p = at(a, 0, 0, 0);
-    *p = *p + v;
+  __device__ __forceinline__ double read(int a, int dx, int dy, int dz) const { return __ldg(at(a, dx, dy, dz)); }
+  __device__ __forceinline__ void write(int a, double v) const { *c[a] = v; }
+  __device__ __forceinline__ void increment(int a, double v) const { *c[a] = __ldg(c[a]) + v; }
+  __device__ __forceinline__ void contribute(double v) {
+    if (L.masked && (px < L.mlo[0] || px >= L.mhi[0] || py < L.mlo[1] || py >= L.mhi[1] || pz < L.mlo[2] ||
+                     pz >= L.mhi[2]))
+      return;
+    acc = red_combine(L.red_op, acc, v);
   }
-  __device__ __forceinline__ void contribute(double v) { acc = red_combine(L.red_op, acc, v); }
   __device__ __forceinline__ int nargs() const { return L.nargs; }
   __device__ __forceinline__ int mode(int a) const { return L.a[a].mode; }
   __device__ __forceinline__ int npts(int a) const { return L.st.npts[L.a[a].stencil]; }
@@ -117,21 +140,57 @@ struct GAcc {
   __device__ __forceinline__ bool reduces() const { return L.has_red != 0; }
 };
 
+// Rows (2D: y, 3D: z) walked by one thread of the untiled executor.
+constexpr int kUntiledRun = 4;
+
 template <int DIM, int BODY>
 __global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch L) {
-  int64_t x, y = 0, z = 0;
-  bool active;
+  GAcc acc{L, {}, 0, 0, 0, red_identity(L.red_op)};
   if (DIM == 1) {
-    x = L.lo[0] + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    active = x < L.lo[0] + L.n[0];
+    acc.px = L.lo[0] + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (acc.px < L.lo[0] + L.n[0]) {
+      acc.locate();
+      tcb::run_body(BODY, acc, L.prm);
+    }
   } else {
-    x = L.lo[0] + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    y = L.lo[1] + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
-    if (DIM == 3) z = L.lo[2] + blockIdx.z;
-    active = x < L.lo[0] + L.n[0] && y < L.lo[1] + L.n[1];
+    acc.px = L.lo[0] + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int64_t r0, rend;
+    if (DIM == 2) {
+      r0 = L.lo[1] + (static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y) * kUntiledRun;
+      rend = L.lo[1] + L.n[1];
+      acc.py = r0;
+    } else {
+      acc.py = L.lo[1] + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+      r0 = L.lo[2] + static_cast<int64_t>(blockIdx.z) * kUntiledRun;
+      rend = L.lo[2] + L.n[2];
+      acc.pz = r0;
+    }
+    const bool active = acc.px < L.lo[0] + L.n[0] && (DIM == 2 || acc.py < L.lo[1] + L.n[1]);
+    if (active) {
+      acc.locate();
+      const int nr = static_cast<int>(min(static_cast<int64_t>(kUntiledRun), rend - r0));
+      if (nr == kUntiledRun) {
+#pragma unroll
+        for (int k = 0; k < kUntiledRun; ++k) {
+          tcb::run_body(BODY, acc, L.prm);
+          acc.advance<DIM>();
+          if (DIM == 2)
+            ++acc.py;
+          else
+            ++acc.pz;
+        }
+      } else {
+        for (int k = 0; k < nr; ++k) {
+          tcb::run_body(BODY, acc, L.prm);
+          acc.advance<DIM>();
+          if (DIM == 2)
+            ++acc.py;
+          else
+            ++acc.pz;
+        }
+      }
+    }
   }
-  GAcc acc{L, x, y, z, red_identity(L.red_op)};
-  if (active) tcb::run_body(BODY, acc, L.prm);
   if (L.has_red) {
     const double v = block_reduce(acc.acc, L.red_op);
     if (threadIdx.x == 0 && threadIdx.y == 0)
@@ -223,6 +282,8 @@ DeviceExec::~DeviceExec() {
   if (scratch_) cudaFree(scratch_);
   if (partials_) cudaFree(partials_);
   if (red_dev_) cudaFree(red_dev_);
+  if (staging_) cudaFree(staging_);
+  if (redbuf_) cudaFree(redbuf_);
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
 }
 
@@ -294,6 +355,84 @@ void DeviceExec::put_point(int f, const Point& p, double val) {
 }
 
 namespace {
+// A dense or pitched buffer: element (ox, oy, oz) at base, `pitch` elements
+// per row, `rows` rows per plane.
+struct BoxBuf {
+  double* base;
+  int64_t ox, oy, oz, pitch, rows;
+};
+
+int64_t lo_of(const Range& r, int d) { return d < r.dim() ? r.start(d) : 0; }
+int64_t ext_of(const Range& r, int d) { return d < r.dim() ? r.extent(d) : 1; }
+
+BoxBuf dense_buf(double* p, const Range& over) {
+  return BoxBuf{p, lo_of(over, 0), lo_of(over, 1), lo_of(over, 2), ext_of(over, 0), ext_of(over, 1)};
+}
+
+void copy_box(const BoxBuf& dst, const BoxBuf& src, const Range& box, cudaStream_t st) {
+  if (box.empty()) return;
+  cudaMemcpy3DParms p{};
+  p.srcPtr = make_cudaPitchedPtr(src.base, static_cast<size_t>(src.pitch) * 8, static_cast<size_t>(src.pitch) * 8,
+                                 static_cast<size_t>(src.rows));
+  p.dstPtr = make_cudaPitchedPtr(dst.base, static_cast<size_t>(dst.pitch) * 8, static_cast<size_t>(dst.pitch) * 8,
+                                 static_cast<size_t>(dst.rows));
+  p.srcPos = make_cudaPos(static_cast<size_t>(lo_of(box, 0) - src.ox) * 8, static_cast<size_t>(lo_of(box, 1) - src.oy),
+                          static_cast<size_t>(lo_of(box, 2) - src.oz));
+  p.dstPos = make_cudaPos(static_cast<size_t>(lo_of(box, 0) - dst.ox) * 8, static_cast<size_t>(lo_of(box, 1) - dst.oy),
+                          static_cast<size_t>(lo_of(box, 2) - dst.oz));
+  p.extent = make_cudaExtent(static_cast<size_t>(ext_of(box, 0)) * 8, static_cast<size_t>(ext_of(box, 1)),
+                             static_cast<size_t>(ext_of(box, 2)));
+  p.kind = cudaMemcpyDefault;
+  TCG_CK(cudaMemcpy3DAsync(&p, st));
+}
+}  // namespace
+
+void DeviceExec::field_to_buf(int f, const Range& box, double* buf, const Range& buf_box) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  if (!b->alloc.contains(box) || !buf_box.contains(box))
+    throw AccessError("field_to_buf: box " + box.to_string() + " outside " + b->alloc.to_string() + " or " +
+                      buf_box.to_string());
+  const BoxBuf fb{b->mem[b->cur], b->x0, lo_of(b->alloc, 1), lo_of(b->alloc, 2), b->py, b->ny};
+  copy_box(dense_buf(buf, buf_box), fb, box, static_cast<cudaStream_t>(stream_));
+}
+
+void DeviceExec::buf_to_field(int f, const Range& box, const double* buf, const Range& buf_box) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  if (!b->alloc.contains(box) || !buf_box.contains(box))
+    throw AccessError("buf_to_field: box " + box.to_string() + " outside " + b->alloc.to_string() + " or " +
+                      buf_box.to_string());
+  const BoxBuf fb{b->mem[b->cur], b->x0, lo_of(b->alloc, 1), lo_of(b->alloc, 2), b->py, b->ny};
+  copy_box(fb, dense_buf(const_cast<double*>(buf), buf_box), box, static_cast<cudaStream_t>(stream_));
+}
+
+double* DeviceExec::staging(size_t n) {
+  if (n > staging_n_) {
+    if (staging_) TCG_CK(cudaFree(staging_));
+    staging_n_ = std::max(n, staging_n_ * 2);
+    TCG_CK(cudaMalloc(&staging_, staging_n_ * sizeof(double)));
+  }
+  return staging_;
+}
+
+void DeviceExec::h2d(double* dev, const double* host, size_t n) {
+  TCG_CK(cudaMemcpyAsync(dev, host, n * sizeof(double), cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream_)));
+}
+
+void DeviceExec::d2h(double* host, const double* dev, size_t n) {
+  TCG_CK(cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream_)));
+  TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+}
+
+double* DeviceExec::red_buffer(size_t n) {
+  if (n > redbuf_n_) {
+    if (redbuf_) TCG_CK(cudaFree(redbuf_));
+    redbuf_n_ = std::max<size_t>(n, 64);
+    TCG_CK(cudaMalloc(&redbuf_, redbuf_n_ * sizeof(double)));
+  }
+  return redbuf_;
+}
+
+namespace {
 void copy2d(DeviceExec& ex, int f, double* dev, int64_t x0, int64_t py, const Range& alloc, double* host, bool up,
             bool async, cudaStream_t st) {
   const int64_t nx = alloc.extent(0);
@@ -343,6 +482,20 @@ void* DeviceExec::take_event() {
   TCG_CK(cudaEventCreate(&e));
   return e;
 }
+
+void* DeviceExec::record() {
+  void* e = take_event();
+  TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e), static_cast<cudaStream_t>(stream_)));
+  return e;
+}
+
+bool DeviceExec::elapsed_ms(void* a, void* b, float* ms) {
+  if (cudaEventQuery(static_cast<cudaEvent_t>(b)) != cudaSuccess) return false;
+  TCG_CK(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b)));
+  return true;
+}
+
+void DeviceExec::release(void* ev) { ev_pool_.push_back(ev); }
 
 void DeviceExec::set_timing(bool on) {
   timing_ = on;
@@ -462,6 +615,11 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
     L.nargs = lp.nargs;
     L.red_op = lp.red >= 0 ? lp.red_op : 0;
     L.has_red = lp.red >= 0;
+    L.masked = ch.masked && L.has_red;
+    for (int d = 0; d < 3; ++d) {
+      L.mlo[d] = ch.mask[d][0];
+      L.mhi[d] = ch.mask[d][1];
+    }
     int64_t n[3];
     bool empty = false;
     for (int d = 0; d < 3; ++d) {
@@ -483,9 +641,10 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
       grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + 255) / 256)), 1, 1);
     } else {
       block = dim3(32, 8, 1);
+      const int64_t ry = ch.dim == 2 ? 8 * kUntiledRun : 8;  // rows of y per block
       grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + 31) / 32)),
-                  static_cast<unsigned>(std::max<int64_t>(1, (n[1] + 7) / 8)),
-                  static_cast<unsigned>(ch.dim == 3 ? std::max<int64_t>(1, n[2]) : 1));
+                  static_cast<unsigned>(std::max<int64_t>(1, (n[1] + ry - 1) / ry)),
+                  static_cast<unsigned>(ch.dim == 3 ? std::max<int64_t>(1, (n[2] + kUntiledRun - 1) / kUntiledRun) : 1));
     }
     const int64_t nblocks = static_cast<int64_t>(grid.x) * grid.y * grid.z;
     if (L.has_red) L.partials = ensure_partials(static_cast<size_t>(nblocks));

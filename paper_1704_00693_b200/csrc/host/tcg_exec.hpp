@@ -21,6 +21,10 @@ struct DevChain {
   std::vector<DatasetId> dat_ids;  // slot -> dataset
   int nred = 0;
   std::vector<int32_t> red_op;     // per reduction index
+  // Reduction mask (execute_plan's reduction_mask, executor.cpp:209-250):
+  // when set, only points inside contribute (a rank's owned box).
+  bool masked = false;
+  int64_t mask[3][2] = {{0, 1}, {0, 1}, {0, 1}};
 };
 
 struct DeviceInfo {
@@ -62,6 +66,18 @@ class DeviceExec {
   int64_t field_bytes(int f) const;
   double get_point(int f, const Point& p);
   void put_point(int f, const Point& p, double v);
+  // Box copies (stream-ordered) between field f's current buffer and a dense
+  // buffer laid out over buf_box (dim 0 fastest), host or device memory.
+  void field_to_buf(int f, const Range& box, double* buf, const Range& buf_box);
+  void buf_to_field(int f, const Range& box, const double* buf, const Range& buf_box);
+  // Device staging for halo messages: >= n doubles, valid until the next
+  // call that needs more.
+  double* staging(size_t n);
+  // Device buffer for reduction partials exchanged between processes.
+  double* red_buffer(size_t n);
+  // Stream-ordered small copies; d2h synchronizes the stream.
+  void h2d(double* dev, const double* host, size_t n);
+  void d2h(double* host, const double* dev, size_t n);
 
   // Execute a lowered chain loop by loop (reference execute_untiled,
   // executor.cpp:252-277). Reductions land in red_out (host) when the call
@@ -77,6 +93,11 @@ class DeviceExec {
   // kernel (k_tiled, k_untiled) on the executor stream; kernel_ms() syncs and
   // returns the accumulated device time and launch count since the last reset.
   void set_timing(bool on);
+  // Chain-level interval timing for the auto executor choice: record() returns
+  // an event recorded on the stream; elapsed_ms(a, b) is valid once b completed.
+  void* record();
+  bool elapsed_ms(void* a, void* b, float* ms);
+  void release(void* ev);
   void kernel_ms(double* tiled_ms, int64_t* tiled_n, double* untiled_ms, int64_t* untiled_n);
   // Bytes of dynamic shared memory available for windows for a chain shape.
   int64_t window_budget_doubles(int nloops, int nred, int ctas_per_sm) const;
@@ -93,6 +114,10 @@ class DeviceExec {
   double* partials_ = nullptr;
   size_t partials_n_ = 0;
   double* red_dev_ = nullptr;
+  double* staging_ = nullptr;
+  size_t staging_n_ = 0;
+  double* redbuf_ = nullptr;
+  size_t redbuf_n_ = 0;
   std::vector<std::pair<uint64_t, PlanBufs*>> plan_cache_;
   int64_t launches_ = 0;
   bool timing_ = false;

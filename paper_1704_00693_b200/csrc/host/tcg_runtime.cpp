@@ -50,6 +50,7 @@ std::string ExecutionReport::to_text() const {
   char b[192];
   auto kv = [&](const char* k, const std::string& v) { o += std::string(k) + "=" + v + "\n"; };
   kv("tiled", tiled ? "1" : "0");
+  kv("executor", executor);
   kv("distributed", distributed ? "1" : "0");
   if (tiled) {
     std::string ts, sk, gr;
@@ -205,7 +206,7 @@ ExecutionReport Runtime::flush(const ExecMode& mode) {
   return execute_chain(take_pending(), mode);
 }
 
-DevChain Runtime::lower(const LoopChain& chain, std::vector<ReductionHandle>& handles) const {
+DevChain Runtime::lower(const LoopChain& chain, const Target& t) const {
   DevChain dc;
   dc.dim = chain.dim;
   std::vector<int> slot;
@@ -218,7 +219,6 @@ DevChain Runtime::lower(const LoopChain& chain, std::vector<ReductionHandle>& ha
       d.red = dc.nred++;
       d.red_op = static_cast<int32_t>(lp.reduction->op);
       dc.red_op.push_back(d.red_op);
-      handles.push_back(lp.reduction->handle);
     }
     d.param_off = static_cast<int32_t>(dc.params.size());
     d.nparams = static_cast<int32_t>(lp.kernel.fn.params.size());
@@ -244,10 +244,36 @@ DevChain Runtime::lower(const LoopChain& chain, std::vector<ReductionHandle>& ha
     for (const Point& p : s.points())
       for (int k = 0; k < 3; ++k) dc.st_pts.push_back(static_cast<int32_t>(p[k]));
   }
-  // Map slots to device field indices for the executors.
-  for (DatasetId& ds : dc.dat_ids) ds = fields_[static_cast<size_t>(ds)].dev;
+  // Map slots to the target's device field indices.
+  for (DatasetId& ds : dc.dat_ids) ds = t.dev.at(static_cast<size_t>(ds));
+  if (t.masked) {
+    dc.masked = true;
+    for (int k = 0; k < 3; ++k) {
+      dc.mask[k][0] = k < chain.dim ? t.mask.start(k) : 0;
+      dc.mask[k][1] = k < chain.dim ? t.mask.end(k) : 1;
+    }
+  }
   return dc;
 }
+
+namespace {
+std::vector<ReductionHandle> reduction_handles(const LoopChain& chain) {
+  std::vector<ReductionHandle> h;
+  for (const LoopRecord& lp : chain.loops)
+    if (lp.reduction) h.push_back(lp.reduction->handle);
+  return h;
+}
+uint64_t mask_hash(const Runtime&, bool masked, const Range& m, int dim) {
+  if (!masked) return 0;
+  uint64_t h = 1469598103934665603ull;
+  for (int d = 0; d < dim; ++d)
+    for (int64_t v : {m.start(d), m.end(d)}) {
+      h ^= static_cast<uint64_t>(v);
+      h *= 1099511628211ull;
+    }
+  return h;
+}
+}  // namespace
 
 void Runtime::store(const std::vector<ReductionHandle>& handles, const double* vals) {
   for (size_t i = 0; i < handles.size(); ++i) {
@@ -258,27 +284,40 @@ void Runtime::store(const std::vector<ReductionHandle>& handles, const double* v
   }
 }
 
-void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep) {
+Runtime::Target Runtime::whole_target() const {
+  Target t;
+  for (const FieldRec& f : fields_) {
+    t.dev.push_back(f.dev);
+    t.alloc.push_back(f.alloc);
+  }
+  return t;
+}
+
+void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep, const Target& t,
+                        std::vector<double>& vals) {
   DeviceExec& dev = device();
   const int s = chain.dim - 1;
   GpuTileChoice choice;
   if (mode.kind == ExecMode::Kind::Tiled) {
+    // Explicit sizes are upper bounds; 0 leaves that dimension to the sizer.
     for (int d = 0; d < chain.dim; ++d) {
+      if (mode.tile_sizes[d] <= 0) continue;
       if (d == s)
-        choice.stream_tile = std::max<int64_t>(1, mode.tile_sizes[d]);
+        choice.stream_tile = mode.tile_sizes[d];
       else
-        choice.block[d] = std::max<int64_t>(1, mode.tile_sizes[d]);
+        choice.block[d] = mode.tile_sizes[d];
     }
   }
   choice.stream_segments = cfg_.stream_segments;
   if (const char* e = std::getenv("TCG_PREFETCH")) choice.prefetch = std::atoi(e);
   if (const char* e = std::getenv("TCG_CTAS_PER_SM")) choice.ctas_per_sm = std::atoi(e);
-  const std::vector<FieldGeom> geoms = field_geoms();
-  const uint64_t sig = chain.signature();
+  std::vector<FieldGeom> geoms;
+  for (const Range& a : t.alloc) geoms.push_back(FieldGeom{a});
+  const uint64_t sig = chain.signature() ^ mask_hash(*this, t.masked, t.mask, chain.dim);
   rep.plan_cache_hit = true;
 
   // Plan of the sub-chain [begin, begin+len); nullptr when its windows do not
-  // fit in shared memory. Cached per (signature, offset, length, mode).
+  // fit in shared memory. Cached per (signature, offset, length, mode, mask).
   auto plan_for = [&](size_t begin, size_t len) -> std::shared_ptr<const GpuTiledPlan> {
     const auto key = std::make_tuple(sig ^ (static_cast<uint64_t>(begin) * 0x9e3779b97f4a7c15ull) ^
                                          (static_cast<uint64_t>(len) << 48),
@@ -295,6 +334,15 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
       const int nl = static_cast<int>(sub.size());
       const WindowBudget budget = [&](int k) { return dev.window_budget_doubles(nl, nred, k); };
       auto p = std::make_shared<GpuTiledPlan>(build_gpu_tiled_plan(sub, geoms, choice, budget, dev.info().num_sms));
+      if (t.masked) {
+        // Reductions count only the target's owned box (execute_plan's
+        // reduction_mask); CTA ownership boxes are only used for that.
+        for (DevCta& c : p->ctas)
+          for (int d = 0; d < chain.dim; ++d) {
+            c.own_lo[d] = static_cast<int32_t>(std::max<int64_t>(c.own_lo[d], t.mask.start(d)));
+            c.own_hi[d] = static_cast<int32_t>(std::min<int64_t>(c.own_hi[d], t.mask.end(d)));
+          }
+      }
       ++gpu_plan_builds_;
       ++rep.plan_constructions;
       rep.plan_seconds += p->build_seconds;
@@ -307,7 +355,7 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
     return gp;
   };
 
-  size_t begin = 0;
+  size_t begin = 0, red_base = 0;
   while (begin < chain.size()) {
     size_t len = chain.size() - begin;
     std::shared_ptr<const GpuTiledPlan> gp = plan_for(begin, len);
@@ -326,12 +374,12 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
       gp = plan_for(begin, len);
     }
     const LoopChain sub = slice(chain, begin, begin + len);
-    std::vector<ReductionHandle> handles;
-    DevChain dc = lower(sub, handles);
-    double vals[kMaxRed] = {0};
+    DevChain dc = lower(sub, t);
+    double sv[kMaxRed] = {0};
     const uint64_t pkey = reinterpret_cast<uint64_t>(gp.get());
-    dev.run_tiled(dc, *gp, pkey, vals);
-    store(handles, vals);
+    dev.run_tiled(dc, *gp, pkey, sv);
+    for (int i = 0; i < dc.nred; ++i) vals.at(red_base + static_cast<size_t>(i)) = sv[i];
+    red_base += static_cast<size_t>(dc.nred);
     last_gpu_plan_ = gp;
     rep.ctas += static_cast<int64_t>(gp->ctas.size());
     rep.computed_points += gp->computed_points;
@@ -346,16 +394,75 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
   }
 }
 
-ExecutionReport Runtime::execute_chain(LoopChain chain, const ExecMode& mode) {
-  const auto t0 = std::chrono::steady_clock::now();
-  ExecutionReport rep;
-  rep.dim = chain.dim;
-  for (const LoopRecord& lp : chain.loops)
-    rep.loops.push_back(LoopExecStats{lp.loop_id, lp.range.volume(), estimate_bytes_moved(lp, lp.range)});
-  ensure_fields();
+std::vector<double> Runtime::run_on(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep,
+                                    const Target& t) {
   DeviceExec& dev = device();
-  const int64_t l0 = dev.launches();
-  if (mode.kind == ExecMode::Kind::Untiled) {
+  size_t nred = 0;
+  for (const LoopRecord& lp : chain.loops) nred += lp.reduction ? 1 : 0;
+  std::vector<double> vals(nred, 0.0);
+  // tiled_auto: choose between the windowed-tiled and the untiled executor by
+  // measured device time of this chain signature, then keep the faster.
+  bool use_untiled = mode.kind == ExecMode::Kind::Untiled;
+  AutoStat* as = nullptr;
+  bool measure = false;
+  if (mode.kind == ExecMode::Kind::TiledAuto) {
+    as = &auto_[chain.signature() ^ mask_hash(*this, t.masked, t.mask, chain.dim)];
+    if (as->ev1) {
+      float ms = 0;
+      if (dev.elapsed_ms(as->ev0, as->ev1, &ms)) {
+        if (as->pending_tiled)
+          as->tiled_ms = std::min(as->tiled_ms, ms);
+        else
+          as->untiled_ms = std::min(as->untiled_ms, ms);
+        dev.release(as->ev0);
+        dev.release(as->ev1);
+        as->ev0 = as->ev1 = nullptr;
+      }
+    }
+    if (!as->ev1) {
+      // Alternate T, U, T, U; each executor's time is the min of its two runs
+      // (the first run of each carries plan construction / lazy module load).
+      const bool t_more = as->tiled_fits && as->tiled_runs < 2;
+      const bool u_more = as->untiled_runs < 2;
+      if (t_more && (as->tiled_runs <= as->untiled_runs || !u_more)) {
+        use_untiled = false;
+        measure = true;
+      } else if (u_more) {
+        use_untiled = true;
+        measure = true;
+      } else {
+        use_untiled = !as->tiled_fits || as->untiled_ms <= as->tiled_ms;
+      }
+    } else {
+      use_untiled = !as->tiled_fits || as->untiled_ms <= as->tiled_ms;
+    }
+    if (measure) {
+      as->ev0 = dev.record();
+      as->pending_tiled = !use_untiled;
+      (use_untiled ? as->untiled_runs : as->tiled_runs)++;
+    }
+  }
+  if (!use_untiled) {
+    try {
+      rep.tiled = true;
+      rep.executor = "tiled";
+      run_tiled(chain, mode, rep, t, vals);
+    } catch (const PlanError& e) {
+      // Chains the windowed executor cannot tile at all (e.g. more than 32
+      // datasets) run untiled under tiled_auto; explicit tiled modes raise.
+      if (mode.kind != ExecMode::Kind::TiledAuto || std::string(e.what()).find("does not fit") == std::string::npos)
+        throw;
+      as->tiled_fits = false;
+      rep.tiled = false;
+      use_untiled = true;
+    }
+  }
+  if (measure && as && use_untiled && as->pending_tiled) {
+    as->pending_tiled = false;  // fell back: time the untiled run instead
+    as->untiled_runs++;
+  }
+  if (use_untiled) {
+    rep.executor = "untiled";
     // Pad sufficiency of untiled execution: every access of the recorded
     // ranges must stay inside its allocation (the reference's checked
     // accessor would throw AccessError at run time, kernel_ctx.hpp:58-73).
@@ -369,23 +476,288 @@ ExecutionReport Runtime::execute_chain(LoopChain chain, const ExecMode& mode) {
           hi[d] = mode_reads(a.mode) ? std::max<int64_t>(st.max_offset(d), 0) : 0;
         }
         const Range touched = lp.range.dilated(lo, hi);
-        if (!fields_[static_cast<size_t>(a.dataset)].alloc.contains(touched))
+        const Range& alloc = t.alloc.at(static_cast<size_t>(a.dataset));
+        if (!alloc.contains(touched))
           throw AccessError("loop k" + std::to_string(lp.kernel.id) + " (id " + std::to_string(lp.loop_id) +
                             "), dataset " + fields_[static_cast<size_t>(a.dataset)].name + ": access over " +
-                            touched.to_string() + " outside allocated extent " +
-                            fields_[static_cast<size_t>(a.dataset)].alloc.to_string());
+                            touched.to_string() + " outside allocated extent " + alloc.to_string());
       }
     }
-    std::vector<ReductionHandle> handles;
-    DevChain dc = lower(chain, handles);
-    std::vector<double> vals(static_cast<size_t>(std::max(1, dc.nred)));
-    dev.run_untiled(dc, vals.data());
-    store(handles, vals.data());
-    rep.tiles_executed = 1;
-  } else {
-    rep.tiled = true;
-    run_tiled(chain, mode, rep);
+    DevChain dc = lower(chain, t);
+    std::vector<double> out(static_cast<size_t>(std::max(1, dc.nred)));
+    dev.run_untiled(dc, out.data());
+    for (size_t i = 0; i < nred; ++i) vals[i] = out[i];
+    rep.tiles_executed += 1;
   }
+  if (measure && as) as->ev1 = dev.record();
+  return vals;
+}
+
+ExecutionReport Runtime::execute_chain(LoopChain chain, const ExecMode& mode) {
+  if (distributed()) return execute_distributed(std::move(chain), mode);
+  const auto t0 = std::chrono::steady_clock::now();
+  ExecutionReport rep;
+  rep.dim = chain.dim;
+  for (const LoopRecord& lp : chain.loops)
+    rep.loops.push_back(LoopExecStats{lp.loop_id, lp.range.volume(), estimate_bytes_moved(lp, lp.range)});
+  ensure_fields();
+  DeviceExec& dev = device();
+  const int64_t l0 = dev.launches();
+  const std::vector<double> vals = run_on(chain, mode, rep, whole_target());
+  store(reduction_handles(chain), vals.data());
+  rep.launches = dev.launches() - l0;
+  rep.exec_seconds = secs_since(t0) - rep.plan_seconds;
+  rep.total_seconds = secs_since(t0);
+  last_report_ = rep;
+  return rep;
+}
+
+// ---- distribution -------------------------------------------------------------
+
+void Runtime::set_rank_grid(const std::array<int, kMaxDims>& grid) {
+  // runtime.cpp:213-222
+  for (int d = 0; d < kMaxDims; ++d) {
+    if (grid[d] < 1) throw InvalidArgument("set_rank_grid: grid entries must be >= 1");
+    if (d >= dim_ && grid[d] != 1) throw InvalidArgument("set_rank_grid: grid uses dimension beyond block");
+  }
+  flush();
+  drop_dist();
+  comm_.reset();
+  grid_ = grid;
+  grid_set_ = true;
+  proc_rank_ = -1;
+}
+
+void Runtime::set_process_rank(const std::array<int, kMaxDims>& grid, int rank, const uint8_t id[kCommIdBytes]) {
+  for (int d = 0; d < kMaxDims; ++d) {
+    if (grid[d] < 1) throw InvalidArgument("set_process_rank: grid entries must be >= 1");
+    if (d >= dim_ && grid[d] != 1) throw InvalidArgument("set_process_rank: grid uses dimension beyond block");
+  }
+  const int n = grid[0] * grid[1] * grid[2];
+  if (rank < 0 || rank >= n) throw InvalidArgument("set_process_rank: rank out of range");
+  flush();
+  drop_dist();
+  device();  // the communicator binds to the current device
+  comm_.reset();
+  comm_ = std::make_unique<Comm>(n, rank, id);
+  grid_ = grid;
+  grid_set_ = true;
+  proc_rank_ = rank;
+}
+
+const RankLayout& Runtime::rank_layout() {
+  if (!grid_set_) throw InvalidArgument("rank_layout: no rank grid set");
+  if (dist_) return dist_->layout;
+  static thread_local RankLayout lay;
+  if (fields_.empty()) throw InvalidArgument("distributed execution requires declared fields");
+  Range global = fields_[0].logical;
+  for (const FieldRec& f : fields_) global = global.hull(f.logical);
+  lay = decompose(global, grid_);
+  return lay;
+}
+
+void Runtime::drop_dist() {
+  if (!dist_) return;
+  // Carry rank data back into the undistributed fields (the reference gathers
+  // after every distributed flush, runtime.cpp:128-137).
+  ensure_fields();
+  DeviceExec& dev = device();
+  for (size_t ds = 0; ds < fields_.size(); ++ds) {
+    const FieldRec& f = fields_[ds];
+    std::vector<double> host(static_cast<size_t>(f.alloc.volume()));
+    download(static_cast<DatasetId>(ds), host.data());
+    dev.upload(f.dev, host.data());
+  }
+  dist_.reset();
+}
+
+void Runtime::ensure_dist() {
+  if (dist_ && dist_->targets.size() == static_cast<size_t>(dist_->layout.rank_count()) &&
+      (dist_->local.empty() || dist_->targets[static_cast<size_t>(dist_->local[0])].dev.size() == fields_.size()))
+    return;
+  DeviceExec& dev = device();
+  const bool fresh = !dist_;
+  if (fresh) {
+    auto d = std::make_unique<Dist>();
+    d->layout = rank_layout();
+    const int R = d->layout.rank_count();
+    if (proc_rank_ >= 0) {
+      if (comm_->nranks() != R) throw InvalidArgument("set_process_rank: grid and communicator size differ");
+      d->local = {proc_rank_};
+    } else {
+      for (int r = 0; r < R; ++r) d->local.push_back(r);
+    }
+    d->targets.resize(static_cast<size_t>(R));
+    dist_ = std::move(d);
+  }
+  // Rank fields: owned box +- the field's pad (dist.cpp:519-529), seeded from
+  // the undistributed field when it already holds data (scatter,
+  // dist.cpp:532-545).
+  for (int r : dist_->local) {
+    Target& t = dist_->targets[static_cast<size_t>(r)];
+    t.masked = true;
+    t.mask = dist_->layout.owned[static_cast<size_t>(r)];
+    for (size_t ds = t.dev.size(); ds < fields_.size(); ++ds) {
+      const FieldRec& f = fields_[ds];
+      if (!dist_->layout.global.contains(f.logical))
+        throw InvalidArgument("declare_field: field " + f.name + " lies outside the distributed domain");
+      const Range a = rank_alloc(dist_->layout, r, f.pad);
+      const int idx = dev.add_field(a);
+      t.dev.push_back(idx);
+      t.alloc.push_back(a);
+      if (f.dev >= 0) {
+        const Range box = a.intersect(f.alloc);
+        std::vector<double> tmp(static_cast<size_t>(box.volume()));
+        dev.field_to_buf(f.dev, box, tmp.data(), box);
+        dev.buf_to_field(idx, box, tmp.data(), box);
+        dev.synchronize();
+      }
+    }
+  }
+}
+
+std::shared_ptr<const DistSchedule> Runtime::dist_schedule(const LoopChain& chain) {
+  const auto key = std::make_pair(chain.signature(), dist_->hist_version);
+  auto it = dist_->schedules.find(key);
+  if (it != dist_->schedules.end()) return it->second;
+  std::vector<int64_t> pads;
+  for (const FieldRec& f : fields_) pads.push_back(f.pad);
+  auto s = std::make_shared<const DistSchedule>(
+      build_dist_schedule(chain, dist_->layout, pads, &dist_->written));
+  dist_->schedules[key] = s;
+  return s;
+}
+
+DistSchedule Runtime::schedule_pending() {
+  if (!grid_set_) throw InvalidArgument("schedule_pending: no rank grid set");
+  LoopChain chain = take_pending();
+  if (!dist_) {
+    // Host-only use (no device): layout and history without rank fields.
+    auto d = std::make_unique<Dist>();
+    d->layout = rank_layout();
+    dist_ = std::move(d);
+  }
+  std::vector<int64_t> pads;
+  for (const FieldRec& f : fields_) pads.push_back(f.pad);
+  DistSchedule s = build_dist_schedule(chain, dist_->layout, pads, &dist_->written);
+  if (note_writes(dist_->written, chain)) ++dist_->hist_version;
+  return s;
+}
+
+void Runtime::exchange(const DistSchedule& s, ExecutionReport& rep) {
+  DeviceExec& dev = device();
+  std::vector<char> is_local(static_cast<size_t>(dist_->layout.rank_count()), 0);
+  for (int r : dist_->local) is_local[static_cast<size_t>(r)] = 1;
+  for (int d = 0; d < kMaxDims; ++d) {
+    const size_t a = s.phase[static_cast<size_t>(d)], b = s.phase[static_cast<size_t>(d) + 1];
+    if (a == b) continue;
+    // Staging offsets of the messages this process takes part in.
+    std::vector<size_t> off(b - a, 0);
+    size_t total = 0;
+    for (size_t i = a; i < b; ++i) {
+      const HaloMsg& m = s.msgs[i];
+      if (!is_local[static_cast<size_t>(m.src)] && !is_local[static_cast<size_t>(m.dst)]) continue;
+      off[i - a] = total;
+      total += static_cast<size_t>(m.points);
+    }
+    if (total == 0) continue;
+    double* stg = dev.staging(total);
+    // Pack every message whose source rank lives here.
+    for (size_t i = a; i < b; ++i) {
+      const HaloMsg& m = s.msgs[i];
+      if (!is_local[static_cast<size_t>(m.src)]) continue;
+      const Target& t = dist_->targets[static_cast<size_t>(m.src)];
+      dev.field_to_buf(t.dev[static_cast<size_t>(m.ds)], m.box, stg + off[i - a], m.box);
+    }
+    // Carry the remote ones (one NCCL group per dimension phase).
+    if (comm_) {
+      bool any = false;
+      for (size_t i = a; i < b && !any; ++i)
+        any = is_local[static_cast<size_t>(s.msgs[i].src)] != is_local[static_cast<size_t>(s.msgs[i].dst)];
+      if (any) {
+        comm_->group_start();
+        for (size_t i = a; i < b; ++i) {
+          const HaloMsg& m = s.msgs[i];
+          const bool ls = is_local[static_cast<size_t>(m.src)], ld = is_local[static_cast<size_t>(m.dst)];
+          if (ls && !ld) comm_->send(stg + off[i - a], static_cast<size_t>(m.points), m.dst, dev.stream());
+          if (ld && !ls) comm_->recv(stg + off[i - a], static_cast<size_t>(m.points), m.src, dev.stream());
+        }
+        comm_->group_end();
+      }
+    }
+    // Unpack every message whose destination rank lives here.
+    for (size_t i = a; i < b; ++i) {
+      const HaloMsg& m = s.msgs[i];
+      if (!is_local[static_cast<size_t>(m.dst)]) continue;
+      const Target& t = dist_->targets[static_cast<size_t>(m.dst)];
+      dev.buf_to_field(t.dev[static_cast<size_t>(m.ds)], m.box, stg + off[i - a], m.box);
+    }
+  }
+  rep.halo_messages = static_cast<int64_t>(s.msgs.size());
+  rep.halo_bytes = s.message_bytes;
+  rep.halo_exchanges = s.msgs.empty() ? 0 : 1;
+}
+
+ExecutionReport Runtime::execute_distributed(LoopChain chain, const ExecMode& mode) {
+  // DistContext::run_tiled (dist.cpp:617-689): plans + halo specs for every
+  // rank, one exchange, per-rank execution with reductions masked to the
+  // owned box, rank-order fold, note_writes.
+  const auto t0 = std::chrono::steady_clock::now();
+  ExecutionReport rep;
+  rep.dim = chain.dim;
+  rep.distributed = true;
+  for (const LoopRecord& lp : chain.loops)
+    rep.loops.push_back(LoopExecStats{lp.loop_id, lp.range.volume(), estimate_bytes_moved(lp, lp.range)});
+  ensure_dist();
+  DeviceExec& dev = device();
+  const int64_t l0 = dev.launches();
+  const auto sched = dist_schedule(chain);
+  exchange(*sched, rep);
+  const std::vector<ReductionHandle> handles = reduction_handles(chain);
+  std::vector<ReduceOp> ops;
+  for (const LoopRecord& lp : chain.loops)
+    if (lp.reduction) ops.push_back(lp.reduction->op);
+  const size_t nred = ops.size();
+  const int R = dist_->layout.rank_count();
+  std::vector<double> part(static_cast<size_t>(R) * nred, 0.0);
+  std::string executor;
+  for (int r : dist_->local) {
+    const LoopChain lc = with_ranges(chain, sched->ranks[static_cast<size_t>(r)].loop_ranges);
+    ExecutionReport rr;
+    rr.dim = chain.dim;
+    const std::vector<double> v = run_on(lc, mode, rr, dist_->targets[static_cast<size_t>(r)]);
+    for (size_t i = 0; i < nred; ++i) part[static_cast<size_t>(r) * nred + i] = v[i];
+    rep.tiled = rep.tiled || rr.tiled;
+    executor = executor.empty() || executor == rr.executor ? rr.executor : "mixed";
+    rep.ctas += rr.ctas;
+    rep.subchains += rr.subchains;
+    rep.tiles_executed += rr.tiles_executed;
+    rep.plan_constructions += rr.plan_constructions;
+    rep.plan_seconds += rr.plan_seconds;
+    rep.computed_points += rr.tiled ? rr.computed_points : sched->ranks[static_cast<size_t>(r)].computed_points;
+    for (int d = 0; d < chain.dim; ++d) {
+      rep.max_skew[d] = std::max(rep.max_skew[d], rr.max_skew[d]);
+      rep.tile_sizes[d] = rr.tile_sizes[d];
+      rep.cta_grid[d] = rr.cta_grid[d];
+    }
+  }
+  rep.executor = executor;
+  if (comm_ && nred > 0) {
+    // Every rank's partials to every process, then the same rank-order fold.
+    double* buf = dev.red_buffer((static_cast<size_t>(R) + 1) * nred);
+    const size_t me = static_cast<size_t>(proc_rank_);
+    dev.h2d(buf, part.data() + me * nred, nred);
+    comm_->all_gather(buf, buf + nred, nred, dev.stream());
+    dev.d2h(part.data(), buf + nred, static_cast<size_t>(R) * nred);
+  }
+  std::vector<double> vals(nred);
+  for (size_t i = 0; i < nred; ++i) {
+    double acc = reduce_identity(ops[i]);
+    for (int r = 0; r < R; ++r) acc = reduce_combine(ops[i], acc, part[static_cast<size_t>(r) * nred + i]);
+    vals[i] = acc;
+  }
+  store(handles, vals.data());
+  if (note_writes(dist_->written, chain)) ++dist_->hist_version;
   rep.launches = dev.launches() - l0;
   rep.exec_seconds = secs_since(t0) - rep.plan_seconds;
   rep.total_seconds = secs_since(t0);
@@ -418,46 +790,121 @@ double Runtime::fetch_reduction(ReductionHandle h) {
   return slot.value;
 }
 
+// Host access. Distributed: a point is read from its owning rank (padding
+// points from the lowest rank whose allocation holds them); writes go to every
+// local rank whose allocation holds the point, so replicated halo copies stay
+// consistent (the reference re-scatters the global picture each flush,
+// dist.cpp:532-545).
+int Runtime::root_for(DatasetId ds, const Point& p) {
+  const RankLayout& lay = dist_->layout;
+  for (int r = 0; r < lay.rank_count(); ++r)
+    if (lay.owned[static_cast<size_t>(r)].contains(p)) return r;
+  const int64_t pad = fields_.at(static_cast<size_t>(ds)).pad;
+  for (int r = 0; r < lay.rank_count(); ++r)
+    if (rank_alloc(lay, r, pad).contains(p)) return r;
+  throw AccessError("point outside allocated extent " + fields_.at(static_cast<size_t>(ds)).alloc.to_string());
+}
+
 double Runtime::get(DatasetId ds, const Point& p) {
   flush();
-  ensure_fields();
-  return device().get_point(fields_.at(static_cast<size_t>(ds)).dev, p);
+  if (!distributed()) {
+    ensure_fields();
+    return device().get_point(fields_.at(static_cast<size_t>(ds)).dev, p);
+  }
+  ensure_dist();
+  const int root = root_for(ds, p);
+  double v = 0;
+  const Target& t = dist_->targets[static_cast<size_t>(root)];
+  const bool local = !t.dev.empty();
+  if (local) v = device().get_point(t.dev.at(static_cast<size_t>(ds)), p);
+  if (comm_) {
+    DeviceExec& dev = device();
+    double* buf = dev.red_buffer(1);
+    if (local) dev.h2d(buf, &v, 1);
+    comm_->broadcast(buf, 1, root, dev.stream());
+    dev.d2h(&v, buf, 1);
+  }
+  return v;
 }
 
 void Runtime::put(DatasetId ds, const Point& p, double v) {
   flush();
-  ensure_fields();
-  device().put_point(fields_.at(static_cast<size_t>(ds)).dev, p, v);
+  if (!distributed()) {
+    ensure_fields();
+    device().put_point(fields_.at(static_cast<size_t>(ds)).dev, p, v);
+    return;
+  }
+  ensure_dist();
+  if (!fields_.at(static_cast<size_t>(ds)).alloc.contains(p))
+    throw AccessError("point outside allocated extent " + fields_.at(static_cast<size_t>(ds)).alloc.to_string());
+  for (int r : dist_->local) {
+    const Target& t = dist_->targets[static_cast<size_t>(r)];
+    if (t.alloc[static_cast<size_t>(ds)].contains(p)) device().put_point(t.dev[static_cast<size_t>(ds)], p, v);
+  }
 }
 
 void Runtime::upload(DatasetId ds, const double* host) {
   flush();
-  ensure_fields();
-  device().upload(fields_.at(static_cast<size_t>(ds)).dev, host);
+  const FieldRec& f = fields_.at(static_cast<size_t>(ds));
+  if (!distributed()) {
+    ensure_fields();
+    device().upload(f.dev, host);
+    return;
+  }
+  ensure_dist();
+  DeviceExec& dev = device();
+  for (int r : dist_->local) {
+    const Target& t = dist_->targets[static_cast<size_t>(r)];
+    dev.buf_to_field(t.dev[static_cast<size_t>(ds)], t.alloc[static_cast<size_t>(ds)].intersect(f.alloc), host,
+                     f.alloc);
+  }
+  dev.synchronize();
 }
 
 void Runtime::download(DatasetId ds, double* host) {
   flush();
-  ensure_fields();
-  device().download(fields_.at(static_cast<size_t>(ds)).dev, host);
+  const FieldRec& f = fields_.at(static_cast<size_t>(ds));
+  if (!distributed()) {
+    ensure_fields();
+    device().download(f.dev, host);
+    return;
+  }
+  ensure_dist();
+  DeviceExec& dev = device();
+  // Halo/padding copies first, then every owned box (gather, dist.cpp:604-615).
+  for (int r : dist_->local) {
+    const Target& t = dist_->targets[static_cast<size_t>(r)];
+    dev.field_to_buf(t.dev[static_cast<size_t>(ds)], t.alloc[static_cast<size_t>(ds)].intersect(f.alloc), host,
+                     f.alloc);
+  }
+  for (int r : dist_->local) {
+    const Target& t = dist_->targets[static_cast<size_t>(r)];
+    dev.field_to_buf(t.dev[static_cast<size_t>(ds)], dist_->layout.owned[static_cast<size_t>(r)].intersect(f.logical),
+                     host, f.alloc);
+  }
+  dev.synchronize();
 }
 
 void Runtime::fill_logical(DatasetId ds, double v) {
   flush();
-  ensure_fields();
   const FieldRec& f = fields_.at(static_cast<size_t>(ds));
-  std::vector<double> h(static_cast<size_t>(f.alloc.volume()));
-  device().download(f.dev, h.data());
-  const int64_t nx = f.alloc.extent(0);
-  const int64_t ny = dim_ > 1 ? f.alloc.extent(1) : 1;
-  for (int64_t z = dim_ > 2 ? f.logical.start(2) : 0; z < (dim_ > 2 ? f.logical.end(2) : 1); ++z)
-    for (int64_t y = dim_ > 1 ? f.logical.start(1) : 0; y < (dim_ > 1 ? f.logical.end(1) : 1); ++y)
-      for (int64_t x = f.logical.start(0); x < f.logical.end(0); ++x) {
-        const int64_t i = (x - f.alloc.start(0)) + nx * ((dim_ > 1 ? y - f.alloc.start(1) : 0) +
-                                                          ny * (dim_ > 2 ? z - f.alloc.start(2) : 0));
-        h[static_cast<size_t>(i)] = v;
-      }
-  device().upload(f.dev, h.data());
+  DeviceExec& dev = device();
+  auto fill = [&](int idx, const Range& box) {
+    if (box.empty()) return;
+    std::vector<double> h(static_cast<size_t>(box.volume()), v);
+    dev.buf_to_field(idx, box, h.data(), box);
+    dev.synchronize();
+  };
+  if (!distributed()) {
+    ensure_fields();
+    fill(f.dev, f.logical);
+    return;
+  }
+  ensure_dist();
+  for (int r : dist_->local) {
+    const Target& t = dist_->targets[static_cast<size_t>(r)];
+    fill(t.dev[static_cast<size_t>(ds)], t.alloc[static_cast<size_t>(ds)].intersect(f.logical));
+  }
 }
 
 }  // namespace tcg

@@ -13,6 +13,8 @@
 #include <map>
 #include <memory>
 
+#include "tcg_comm.hpp"
+#include "tcg_dist.hpp"
 #include "tcg_exec.hpp"
 #include "tcg_gpuplan.hpp"
 #include "tcg_plan.hpp"
@@ -62,6 +64,7 @@ struct ExecutionReport {
   int64_t ctas = 0;
   int64_t subchains = 0;
   int64_t computed_points = 0;
+  std::string executor = "untiled";  // executor that ran the chain (tiled_auto may pick either)
   std::array<int, kMaxDims> cta_grid{1, 1, 1};
   int64_t total_points() const;
   int64_t total_bytes_moved() const;
@@ -94,6 +97,19 @@ class Runtime {
   void upload(DatasetId ds, const double* host);
   void download(DatasetId ds, double* host);
 
+  // Distribution over a rank grid (reference Runtime::set_rank_grid,
+  // runtime.hpp:77-81, runtime.cpp:213-222). set_rank_grid hosts every rank
+  // in this process on this GPU (the reference's simulated ranks);
+  // set_process_rank hosts one rank per process, messages over NCCL. Data
+  // already on the device is carried over into the rank fields.
+  void set_rank_grid(const std::array<int, kMaxDims>& grid);
+  void set_process_rank(const std::array<int, kMaxDims>& grid, int rank, const uint8_t id[kCommIdBytes]);
+  bool distributed() const { return grid_set_; }
+  const RankLayout& rank_layout();
+  // Host-only: the distribution schedule of the pending chain (consumed; its
+  // writes are recorded as if it had run). Needs a rank grid, no GPU.
+  DistSchedule schedule_pending();
+
   size_t pending_loops() const { return pending_.size(); }
   LoopChain take_pending();
   const Range& alloc_range(DatasetId ds) const { return fields_.at(static_cast<size_t>(ds)).alloc; }
@@ -124,10 +140,35 @@ class Runtime {
     bool consumed = false;
   };
 
+  // Where a chain executes: the undistributed fields or one rank's fields.
+  struct Target {
+    std::vector<int> dev;      // dataset -> device field index
+    std::vector<Range> alloc;  // dataset -> allocation
+    bool masked = false;       // reductions only over `mask` (the rank's owned box)
+    Range mask;
+  };
+  struct Dist {
+    RankLayout layout;
+    std::vector<int> local;            // ranks hosted by this process
+    std::vector<Target> targets;       // [rank]; filled for local ranks
+    WriteHistory written;              // note_writes history (dist.cpp:590-602)
+    uint64_t hist_version = 0;
+    std::map<std::pair<uint64_t, uint64_t>, std::shared_ptr<const DistSchedule>> schedules;
+  };
+
   ExecutionReport execute_chain(LoopChain chain, const ExecMode& mode);
+  ExecutionReport execute_distributed(LoopChain chain, const ExecMode& mode);
+  std::vector<double> run_on(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep, const Target& t);
   void ensure_fields();
-  DevChain lower(const LoopChain& chain, std::vector<ReductionHandle>& handles) const;
-  void run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep);
+  Target whole_target() const;
+  void ensure_dist();
+  void drop_dist();
+  std::shared_ptr<const DistSchedule> dist_schedule(const LoopChain& chain);
+  void exchange(const DistSchedule& s, ExecutionReport& rep);
+  int root_for(DatasetId ds, const Point& p);
+  DevChain lower(const LoopChain& chain, const Target& t) const;
+  void run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep, const Target& t,
+                 std::vector<double>& vals);
   void store(const std::vector<ReductionHandle>& handles, const double* vals);
 
   int dim_;
@@ -143,7 +184,23 @@ class Runtime {
   int64_t gpu_plan_builds_ = 0;
   std::shared_ptr<const GpuTiledPlan> last_gpu_plan_;
   ExecutionReport last_report_;
+  // tiled_auto: per chain signature, device time of the windowed-tiled and the
+  // untiled executor (both bit-exact); later flushes use the faster one.
+  struct AutoStat {
+    int tiled_runs = 0, untiled_runs = 0;
+    float tiled_ms = 1e30f, untiled_ms = 1e30f;
+    bool tiled_fits = true;
+    void* ev0 = nullptr;
+    void* ev1 = nullptr;
+    bool pending_tiled = false;
+  };
+  std::map<uint64_t, AutoStat> auto_;
+  std::array<int, kMaxDims> grid_{1, 1, 1};
+  bool grid_set_ = false;
+  int proc_rank_ = -1;  // >= 0: one rank per process
+  std::unique_ptr<Dist> dist_;
   std::unique_ptr<DeviceExec> dev_;
+  std::unique_ptr<Comm> comm_;  // destroyed before dev_ (declared after it)
 };
 
 }  // namespace tcg

@@ -298,6 +298,37 @@ int tcg_gpu_plan_pending(tcg_runtime* rt, int mode, const int64_t ts[3], char* b
   });
 }
 
+int tcg_set_rank_grid(tcg_runtime* rt, const int32_t grid[3]) {
+  return guard([&] { rt->rt->set_rank_grid({grid[0], grid[1], grid[2]}); });
+}
+
+int tcg_rank_owned(tcg_runtime* rt, int32_t rank, int64_t out[6]) {
+  return guard([&] {
+    const tcg::RankLayout& lay = rt->rt->rank_layout();
+    if (rank < 0 || rank >= lay.rank_count()) throw tcg::InvalidArgument("rank_owned: rank out of range");
+    const tcg::Range& o = lay.owned[static_cast<size_t>(rank)];
+    for (int d = 0; d < 3; ++d) {
+      out[2 * d] = d < o.dim() ? o.start(d) : 0;
+      out[2 * d + 1] = d < o.dim() ? o.end(d) : 1;
+    }
+  });
+}
+
+int tcg_comm_unique_id(uint8_t out[128]) {
+  return guard([&] { tcg::Comm::unique_id(out); });
+}
+
+int tcg_set_process_rank(tcg_runtime* rt, const int32_t grid[3], int32_t rank, const uint8_t id[128]) {
+  return guard([&] { rt->rt->set_process_rank({grid[0], grid[1], grid[2]}, rank, id); });
+}
+
+int tcg_dist_schedule_pending(tcg_runtime* rt, char* buf, int64_t n, int64_t* needed) {
+  return guard([&] {
+    const tcg::DistSchedule s = rt->rt->schedule_pending();
+    put_text(tcg::schedule_text(s, rt->rt->dim()), buf, n, needed);
+  });
+}
+
 int tcg_signature_pending(tcg_runtime* rt, uint64_t* out) {
   return guard([&] {
     tcg::LoopChain c = rt->rt->take_pending();

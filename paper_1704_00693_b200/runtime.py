@@ -102,6 +102,11 @@ def load_library() -> ctypes.CDLL:
         "tcg_gpu_plan_pending": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I64), ctypes.c_char_p, _I64,
                                                 ctypes.POINTER(_I64)]),
         "tcg_signature_pending": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
+        "tcg_set_rank_grid": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
+        "tcg_rank_owned": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_I64)]),
+        "tcg_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+        "tcg_set_process_rank": (ctypes.c_int, [_P, ctypes.POINTER(_I32), _I32, ctypes.c_char_p]),
+        "tcg_dist_schedule_pending": (ctypes.c_int, [_P, ctypes.c_char_p, _I64, ctypes.POINTER(_I64)]),
         "tcg_auto_tile_size": (ctypes.c_int, [ctypes.c_int, _I64, _I32, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
         "tcg_device_info": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(_I32), ctypes.POINTER(_I64),
                                            ctypes.POINTER(_I64)]),
@@ -248,6 +253,33 @@ class RuntimeConfig:
     stream_segments: int = 0
 
 
+def comm_unique_id() -> bytes:
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.tcg_comm_unique_id(buf))
+    return buf.raw
+
+
+def parse_schedule(text: str, dim: int) -> dict:
+    ranks, msgs = {}, []
+    for line in text.splitlines():
+        f = line.split()
+        if not f:
+            continue
+        kv = {k: v for k, _, v in (x.partition("=") for x in f if "=" in x)}
+        if line.startswith("rank="):
+            ranks[int(kv["rank"])] = {"owned": kv["owned"], "computed": int(kv["computed"]), "loops": []}
+        elif f[0] == "loop":
+            nums = [int(v) for v in f[3:]]
+            ranks[int(kv["rank"])]["loops"].append([(nums[2 * d], nums[2 * d + 1]) for d in range(dim)])
+        elif f[0] == "msg":
+            i = f.index("box")
+            nums = [int(v) for v in f[i + 1:]]
+            msgs.append({"src": int(kv["src"]), "dst": int(kv["dst"]), "ds": int(kv["ds"]), "dim": int(kv["dim"]),
+                         "dir": int(kv["dir"]), "box": [(nums[2 * d], nums[2 * d + 1]) for d in range(dim)]})
+    return {"ranks": ranks, "msgs": msgs}
+
+
 def parse_report(text: str) -> dict:
     rep = {}
     for line in text.splitlines():
@@ -272,6 +304,7 @@ class Runtime:
         self.dim = dim
         self.config = cfg
         self._allocs: list[Range] = []
+        self._logicals: list[Range] = []
 
     def close(self):
         if getattr(self, "_h", None):
@@ -304,10 +337,14 @@ class Runtime:
         a = (_I64 * 6)()
         _check(self._lib.tcg_alloc_range(self._h, out.value, a))
         self._allocs.append(Range(self.dim, list(a)))
+        self._logicals.append(Range(self.dim, logical.lohi))
         return out.value
 
     def alloc_range(self, ds: int) -> Range:
         return self._allocs[ds]
+
+    def logical_range(self, ds: int) -> Range:
+        return self._logicals[ds]
 
     # ---- lazy queue -----------------------------------------------------
     def par_loop(self, kernel: KernelHandle, rng: Range, args: Sequence, reduction: Optional[int] = None) -> int:
@@ -391,6 +428,33 @@ class Runtime:
 
     def gpu_plan_pending(self, mode: ExecMode, size: int = 1 << 26) -> str:
         return _text(self._lib.tcg_gpu_plan_pending, self._h, mode.kind, _arr(_I64, mode.tile_sizes), size=size)
+
+    # ---- distribution ----------------------------------------
+    def set_rank_grid(self, grid):
+        """Runtime::set_rank_grid (runtime.hpp:77-81): every rank hosted in this
+        process on this GPU (the reference's simulated ranks)."""
+        g = list(grid) + [1] * (3 - len(grid))
+        _check(self._lib.tcg_set_rank_grid(self._h, _arr(_I32, g[:3])))
+
+    def set_process_rank(self, grid, rank: int, comm_id: bytes):
+        """One rank per process; comm_id from comm_unique_id() on rank 0."""
+        g = list(grid) + [1] * (3 - len(grid))
+        if len(comm_id) != 128:
+            raise InvalidArgument("set_process_rank: comm_id must be 128 bytes")
+        _check(self._lib.tcg_set_process_rank(self._h, _arr(_I32, g[:3]), rank, comm_id))
+
+    def rank_owned(self, rank: int) -> Range:
+        """Owned box of `rank` in the rank grid's decomposition (decompose,
+        dist.cpp:142-177) of the declared fields' hull."""
+        a = (_I64 * 6)()
+        _check(self._lib.tcg_rank_owned(self._h, rank, a))
+        return Range(self.dim, list(a))
+
+    def schedule_pending(self) -> dict:
+        """Host-only distribution schedule of the pending chain (consumed; its
+        writes are recorded as if executed): per-rank loop ranges and the
+        halo message list in exchange order."""
+        return parse_schedule(_text(self._lib.tcg_dist_schedule_pending, self._h), self.dim)
 
     def signature_pending(self) -> int:
         out = ctypes.c_uint64()

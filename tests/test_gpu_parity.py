@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import chains as C
-from paper_1704_00693_b200 import ExecMode, Runtime, RuntimeConfig, configs
+from paper_1704_00693_b200 import ExecMode, Runtime, RuntimeConfig, configs, parse_report
 
 pytestmark = pytest.mark.gpu
 
@@ -143,3 +143,23 @@ def test_fetch_reduction_flushes_prefix_only():
     assert rt.get(f1, (5,)) == 2.5
     rt.fill_logical(f1, 1.5)
     assert rt.get(f1, (0,)) == 1.5 and rt.get(f1, (-1,)) == 0.0
+
+
+def test_tiled_auto_switches_executor_bit_exact(oracle_lib):
+    # tiled_auto times both executors per chain signature (tiled, untiled,
+    # tiled, untiled) and keeps the faster; every flush must stay bit-exact.
+    steps = 8
+    want = _run_config(oracle_lib.OracleRuntime(2), configs.HydroC2, 96, steps=steps)
+    rt = Runtime(2)
+    rt.set_default_mode(ExecMode.tiled_auto())
+    c = configs.HydroC2(rt, 96)
+    mins, used = [], []
+    for _ in range(steps):
+        mins.append(rt.fetch_reduction(c.enqueue_step()))
+        used.append(parse_report(rt.report_text())["executor"])
+    assert used[:4] == ["tiled", "untiled", "tiled", "untiled"], used
+    assert len(set(used[4:])) == 1, used
+    got = c.outputs()
+    for k in want[0]:
+        assert np.array_equal(got[k], want[0][k]), k
+    assert mins == want[1]
