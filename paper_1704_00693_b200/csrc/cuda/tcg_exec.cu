@@ -743,9 +743,13 @@ void DeviceExec::run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t 
   P.loops = cd.loops;
   P.params = cd.params;
   P.stencils = cd.st;
+  // Device fields come from the lowered chain (the target's field map: the
+  // undistributed fields or one rank's); the plan only knows chain slots.
+  if (ch.dat_ids.size() != static_cast<size_t>(gp.ndat))
+    throw PlanError("tiled executor: chain and plan disagree on the dataset count");
   for (int k = 0; k < gp.ndat; ++k) {
     P.dats[k] = gp.dats[static_cast<size_t>(k)];
-    const int f = gp.dat_ids[static_cast<size_t>(k)];
+    const int f = ch.dat_ids[static_cast<size_t>(k)];
     P.src[k] = view(f, false);
     P.dst[k] = gp.dats[static_cast<size_t>(k)].pingpong ? view(f, true) : P.src[k];
   }
@@ -775,7 +779,7 @@ void DeviceExec::run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t 
   }
   ++launches_;
   for (int k = 0; k < gp.ndat; ++k)
-    if (gp.dats[static_cast<size_t>(k)].pingpong) swap(gp.dat_ids[static_cast<size_t>(k)]);
+    if (gp.dats[static_cast<size_t>(k)].pingpong) swap(ch.dat_ids[static_cast<size_t>(k)]);
   for (int r = 0; r < gp.nred; ++r) {
     k_fold<<<1, 1024, 0, st>>>(P.red_partials + static_cast<int64_t>(r) * P.nctas, P.nctas, P.red_op[r], red_dev_ + r);
     TCG_CK(cudaGetLastError());

@@ -96,6 +96,25 @@ Runtime::Runtime(int dim, RuntimeConfig cfg) : dim_(dim), cfg_(cfg) {
   if (dim < 1 || dim > kMaxDims) throw InvalidArgument("Runtime: block dim must be 1, 2, or 3");
   if (cfg_.threads < 1) throw InvalidArgument("Runtime: threads must be >= 1");
   if (cfg_.skew_allowance < 0) throw InvalidArgument("Runtime: skew_allowance must be >= 0");
+  // tiled_auto decisions persisted across processes (like a library autotune
+  // cache): "signature tiled_ms untiled_ms tiled_fits" per line.
+  if (const char* path = std::getenv("TCG_AUTOTUNE_FILE")) {
+    autotune_file_ = path;
+    if (FILE* f = std::fopen(path, "r")) {
+      unsigned long long sig = 0;
+      float tm = 0, um = 0;
+      int fits = 0;
+      while (std::fscanf(f, "%llx %f %f %d", &sig, &tm, &um, &fits) == 4) {
+        AutoStat& a = auto_[static_cast<uint64_t>(sig)];
+        a.tiled_runs = a.untiled_runs = 2;
+        a.tiled_ms = tm;
+        a.untiled_ms = um;
+        a.tiled_fits = fits != 0;
+        a.saved = true;
+      }
+      std::fclose(f);
+    }
+  }
 }
 
 Runtime::~Runtime() = default;
@@ -394,9 +413,30 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
   }
 }
 
-std::vector<double> Runtime::run_on(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep,
+std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode, ExecutionReport& rep,
                                     const Target& t) {
   DeviceExec& dev = device();
+  // Loops with an empty range do nothing (a reducing one yields the
+  // identity); rank-local chains have them wherever a rank computes none of a
+  // loop. Execute the non-empty ones only.
+  std::vector<double> all_vals;
+  std::vector<int> red_src;  // per reduction of `full`: index into vals, -1 = identity
+  LoopChain chain;
+  chain.dim = full.dim;
+  chain.stencils = full.stencils;
+  {
+    int nr = 0;
+    for (const LoopRecord& lp : full.loops) {
+      const bool empty = lp.range.empty();
+      if (lp.reduction) {
+        all_vals.push_back(reduce_identity(lp.reduction->op));
+        red_src.push_back(empty ? -1 : nr);
+        if (!empty) ++nr;
+      }
+      if (!empty) chain.loops.push_back(lp);
+    }
+  }
+  if (chain.loops.empty()) return all_vals;
   size_t nred = 0;
   for (const LoopRecord& lp : chain.loops) nred += lp.reduction ? 1 : 0;
   std::vector<double> vals(nred, 0.0);
@@ -432,6 +472,7 @@ std::vector<double> Runtime::run_on(const LoopChain& chain, const ExecMode& mode
         measure = true;
       } else {
         use_untiled = !as->tiled_fits || as->untiled_ms <= as->tiled_ms;
+        if (!as->saved) save_autotune(*as);
       }
     } else {
       use_untiled = !as->tiled_fits || as->untiled_ms <= as->tiled_ms;
@@ -490,7 +531,9 @@ std::vector<double> Runtime::run_on(const LoopChain& chain, const ExecMode& mode
     rep.tiles_executed += 1;
   }
   if (measure && as) as->ev1 = dev.record();
-  return vals;
+  for (size_t i = 0; i < red_src.size(); ++i)
+    if (red_src[i] >= 0) all_vals[i] = vals[static_cast<size_t>(red_src[i])];
+  return all_vals;
 }
 
 ExecutionReport Runtime::execute_chain(LoopChain chain, const ExecMode& mode) {
@@ -510,6 +553,18 @@ ExecutionReport Runtime::execute_chain(LoopChain chain, const ExecMode& mode) {
   rep.total_seconds = secs_since(t0);
   last_report_ = rep;
   return rep;
+}
+
+void Runtime::save_autotune(AutoStat& as) {
+  as.saved = true;
+  if (autotune_file_.empty()) return;
+  if (FILE* f = std::fopen(autotune_file_.c_str(), "w")) {
+    for (const auto& [sig, a] : auto_)
+      if (a.saved)
+        std::fprintf(f, "%llx %.6f %.6f %d\n", static_cast<unsigned long long>(sig), a.tiled_ms, a.untiled_ms,
+                     a.tiled_fits ? 1 : 0);
+    std::fclose(f);
+  }
 }
 
 // ---- distribution -------------------------------------------------------------

@@ -193,8 +193,11 @@ class Runtime {
     void* ev0 = nullptr;
     void* ev1 = nullptr;
     bool pending_tiled = false;
+    bool saved = false;  // decision final (and written to TCG_AUTOTUNE_FILE)
   };
+  void save_autotune(AutoStat& as);
   std::map<uint64_t, AutoStat> auto_;
+  std::string autotune_file_;
   std::array<int, kMaxDims> grid_{1, 1, 1};
   bool grid_set_ = false;
   int proc_rank_ = -1;  // >= 0: one rank per process

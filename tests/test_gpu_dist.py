@@ -46,12 +46,12 @@ def test_repeated_chains_use_write_history(oracle_lib, mode):
         ho = C.enqueue(ora, gc)
         hg = C.enqueue(rt, gc)
         rt.flush(mode)
+        rep = parse_report(rt.report_text())
+        assert rep["distributed"] == "1" and int(rep["halo_messages"]) > 0
         ro = [(ora.fetch_reduction(h), op) for h, op in ho]
         rg = [(rt.fetch_reduction(h), op) for h, op in hg]
         C.assert_same(([], rg), ([], ro), "reductions")
     C.assert_same(([rt.download(d) for d in ids], []), ([ora.download(d) for d in ids_o], []), "fields")
-    rep = parse_report(rt.report_text())
-    assert rep["distributed"] == "1"
 
 
 def test_hydro_on_four_ranks_matches_reference_dist(ref_lib):
@@ -82,9 +82,9 @@ def test_heat_on_rank_grid_host_access(oracle_lib):
     for rt_, h in ((ora, ho), (rt, hg)):
         h.enqueue_chain(steps=5)
         rt_.flush(ExecMode.tiled_auto())
-    assert np.array_equal(hg.outputs()["u"], ho.outputs()["u"])
     rep = parse_report(rt.report_text())
     assert int(rep["halo_messages"]) == 2  # u both ways once; v is written first
+    assert np.array_equal(hg.outputs()["u"], ho.outputs()["u"])
     # get/put/fill_logical address the owning rank and every halo copy.
     want = ho.outputs()["u"]
     al = ora.alloc_range(ho.u)

@@ -163,3 +163,18 @@ def test_tiled_auto_switches_executor_bit_exact(oracle_lib):
     for k in want[0]:
         assert np.array_equal(got[k], want[0][k]), k
     assert mins == want[1]
+
+
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((0, 0, 0)), ExecMode.tiled_auto()],
+                         ids=["untiled", "tiled", "auto"])
+def test_empty_range_loops(oracle_lib, mode):
+    # A loop with an empty range does nothing; a reducing one yields the
+    # identity (reduce_identity, types.hpp:272-288).
+    gc = C.generate(77, dim=2, min_loops=4, max_loops=6, extent=(40, 56))
+    lohi, args, _ = gc.loops[1]
+    gc.loops.insert(1, ([lohi[0], lohi[1], 9, 9], args, 1))
+    gc.loops.insert(3, ([5, 5, lohi[2], lohi[3]], args, None))
+    want = C.run(oracle_lib.OracleRuntime(2), gc, None)
+    got = C.run(Runtime(2), gc, mode)
+    C.assert_same(got, want, "empty loops")
+    assert float("inf") in [v for v, _ in got[1]]
