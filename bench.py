@@ -27,7 +27,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -56,57 +55,71 @@ def load_profile_traffic(key):
     return None
 
 
+_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    try:
+        print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    except Exception:
+        pass
+    time.sleep(0.01)
+"""
+
+
 class ClockSampler:
-    """Samples SM clocks and throttle reasons via NVML during the timed region."""
+    """Samples SM clocks and throttle reasons via NVML during the timed region,
+    from a child process (a sampling thread here would compete with the
+    host-side launch loop for the GIL)."""
 
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
     def __init__(self, index):
+        self.index = index
         self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self.nv = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.01)
+        self.proc = None
 
     def __enter__(self):
-        if self.nv:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+        import subprocess
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline().split()
+            if first and first[0] == "max":
+                self.max_mhz = int(first[1])
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self.nv:
-            self.t.join()
+        if not self.proc:
+            return
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.splitlines():
+            f = line.split()
+            if len(f) != 2:
+                continue
+            self.samples.append(int(f[0]))
+            mask = int(f[1])
+            for bit, name in self.REASONS.items():
+                if mask & bit and bit != 0x1:
+                    self.reasons.add(name)
 
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def make_config(name, rt, n=None):
+def make_config(name, rt, n=None, ny=None):
     from paper_1704_00693_b200 import configs
     if name == "c2":
-        return configs.HydroC2(rt, n or 4096)
+        return configs.HydroC2(rt, n or 4096, ny=ny)
     if name == "c1":
         return configs.HeatC1(rt, n or 1024)
     if name == "c3":
@@ -166,6 +179,13 @@ WORKLOAD_TEXT = {
 }
 
 
+def workload_text(name, world):
+    t = WORKLOAD_TEXT[name]
+    if name == "c2" and world > 1:
+        t = t.replace("fp64 4096^2", f"fp64 4096 x {4096 * world} (one 4096^2 slab per GPU, weak scaling)")
+    return t
+
+
 def parse_mode(s):
     from paper_1704_00693_b200 import ExecMode
     if s == "auto":
@@ -174,6 +194,10 @@ def parse_mode(s):
         return ExecMode.untiled()
     if s.startswith("tiled:"):
         return ExecMode.tiled([int(v) for v in s[6:].split(",")])
+    if s == "windowed":
+        return ExecMode.windowed()
+    if s.startswith("windowed:"):
+        return ExecMode.windowed([int(v) for v in s[9:].split(",")])
     raise ValueError(s)
 
 
@@ -221,7 +245,7 @@ def time_steps(rt, step, k):
     return e0.elapsed_time(e1)
 
 
-def cpu_reference(cfg_name, k, warmup, budget_s=120.0, mode_pick=None):
+def cpu_reference(cfg_name, k, warmup, budget_s=120.0, mode_pick=None, ny=None):
     """The unmodified reference (oracle/_ref) on the host cores: best of its
     untiled and tiled_auto modes, a bounded number of steps."""
     sys.path.insert(0, str(REPO / "oracle"))
@@ -237,7 +261,7 @@ def cpu_reference(cfg_name, k, warmup, budget_s=120.0, mode_pick=None):
     for mname, mode in modes:
         rt = pyoracle.RefRuntime(2 if cfg_name != "c3" else 3, threads=threads)
         rt.set_default_mode(mode)
-        cfg = make_config(cfg_name, rt)
+        cfg = make_config(cfg_name, rt, ny=ny)
         st = Step(cfg_name, cfg, rt)
         t0 = time.perf_counter()
         st()  # probe step (also warm-up)
@@ -260,14 +284,16 @@ def cpu_reference(cfg_name, k, warmup, budget_s=120.0, mode_pick=None):
 def run_reference_arm(args, world, rank, dist):
     if rank != 0:
         return 0
-    res, err = cpu_reference(args.config, args.steps + args.warmup, args.warmup, budget_s=args.ref_budget)
+    # Same workload as the B200 arm: at N > 1 c2 is the 4096 x 4096N domain.
+    ny = 4096 * world if (world > 1 and args.config == "c2") else None
+    res, err = cpu_reference(args.config, args.steps + args.warmup, args.warmup, budget_s=args.ref_budget, ny=ny)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": err}))
         return 0
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE shapes)",
-            "config": {"workload": WORKLOAD_TEXT[args.config]}, "impl": "reference", "cpu_baseline": res,
+            "config": {"workload": workload_text(args.config, world)}, "impl": "reference", "cpu_baseline": res,
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -285,10 +311,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-untiled", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=60.0)
+    ap.add_argument("--shard", action="store_true", help="c2: use the sharded (NCCL) path even on one GPU")
     args = ap.parse_args()
-    # >= 3 per the contract; tiled_auto settles its executor choice in 4 flushes.
-    args.warmup = max(5, args.warmup)
+    # >= 3 per the contract; tiled_auto settles its executor choice in 6 flushes.
+    args.warmup = max(7, args.warmup)
 
+    # tiled_auto's per-chain executor choices persist here, so a profiler run
+    # of the same command (kernels serialised, timings distorted) executes
+    # the choices the timed run made.
+    os.environ.setdefault("TCG_AUTOTUNE_FILE", str(REPO / f".tcg_autotune_{args.config}"))
     world, rank, local, dist = dist_setup(args.gpus)
     if args.impl == "reference":
         return run_reference_arm(args, world, rank, dist)
@@ -301,10 +332,24 @@ def main():
     torch.cuda.set_device(local)
     mode = parse_mode(args.mode)
 
+    # N > 1: c2 is decomposed into one 4096^2 slab per GPU along y (weak
+    # scaling, domain 4096 x 4096N) with one deep-halo exchange per chain over
+    # NCCL; the other configs run as independent replicas.
+    sharded = (world > 1 or args.shard) and args.config == "c2"
+
+    def new_comm_id():
+        # One NCCL unique id per communicator (every runtime gets its own).
+        obj = [pkg.comm_unique_id() if rank == 0 else None]
+        if dist is not None:
+            dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
     def build(m):
         rt = Runtime(3 if args.config == "c3" else 2)
+        if sharded:
+            rt.set_process_rank((1, world, 1), rank, new_comm_id())
         rt.set_default_mode(m)
-        cfg = make_config(args.config, rt)
+        cfg = make_config(args.config, rt, ny=4096 * world if sharded else None)
         return rt, cfg, Step(args.config, cfg, rt)
 
     # ---- device-resident throughput (value) ----------------------------------
@@ -320,8 +365,10 @@ def main():
     kt = rt.kernel_timing()
     rt.set_timing(False)
     ms = max_over_ranks(ms, dist)
-    cu = step.cell_updates()
-    value = cu * args.steps * world / (ms / 1e3)
+    # Whole-job cell-updates per step: the sharded domain counts once; each
+    # replica counts its own.
+    cu = step.cell_updates() if sharded else step.cell_updates() * world
+    value = cu * args.steps / (ms / 1e3)
     report = pkg.parse_report(rt.report_text())
 
     # The dominant kernel: tiled_auto may settle on either executor per chain.
@@ -330,8 +377,9 @@ def main():
     kms = kt["tiled_ms"] if tiled else kt["untiled_ms"]
     kn = kt["tiled_launches"] if tiled else kt["untiled_launches"]
     peak, peak_src = load_peaks()
-    alg = step.algorithmic_bytes()
-    comp = step.compulsory_bytes()
+    # Algorithmic bytes of this rank's share (kernel timing is per rank).
+    alg = step.algorithmic_bytes() / (world if sharded else 1)
+    comp = step.compulsory_bytes() / (world if sharded else 1)
     per_launch_alg = alg * args.steps / max(kn, 1)
     avg_ms = kms / max(kn, 1)
     achieved = per_launch_alg / (avg_ms / 1e3) / 1e9 if kn else None
@@ -349,23 +397,25 @@ def main():
     del rt, cfg, step
     fixed = {}
     if not args.no_untiled:
-        for mname in ("untiled", "tiled:0,0,0"):
+        for mname in ("untiled", "tiled:0,0,0", "windowed"):
             if mname == args.mode:
                 continue
             rtu, cfgu, stepu = build(parse_mode(mname))
             for _ in range(args.warmup):
                 stepu()
             msu = time_steps(rtu, stepu, args.steps)
-            fixed[mname] = cu * args.steps * world / (max_over_ranks(msu, dist) / 1e3)
+            fixed[mname] = cu * args.steps / (max_over_ranks(msu, dist) / 1e3)
             del rtu, cfgu, stepu
     untiled_value = fixed.get("untiled", value if args.mode == "untiled" else None)
     tiled_value = fixed.get("tiled:0,0,0")
+    windowed_value = fixed.get("windowed")
 
     # ---- end-to-end through the public API with host buffers --------------------
     e2e = None
     if not args.no_e2e:
         rte, cfge, stepe = build(mode)
         ids = list(cfge.init.keys())
+        boxes = getattr(cfge, "init_box", {})
         host = {}
         for ds in ids:
             t = torch.empty(cfge.init[ds].shape, dtype=torch.float64, pin_memory=True)
@@ -378,15 +428,21 @@ def main():
         barrier(dist)
         t0 = time.perf_counter()
         for ds in ids:
-            rte.upload(ds, host[ds])
+            if ds in boxes and boxes[ds] != rte.alloc_range(ds):
+                rte.upload_box(ds, host[ds], boxes[ds])
+            else:
+                rte.upload(ds, host[ds])
         for _ in range(args.steps):
             stepe()
         for ds in ids:
-            out[ds][...] = rte.download(ds)
+            if ds in boxes and boxes[ds] != rte.alloc_range(ds):
+                rte.download_box(ds, boxes[ds], out=out[ds])
+            else:
+                out[ds][...] = rte.download(ds)
         rte.synchronize()
         dt = max_over_ranks(time.perf_counter() - t0, dist)
-        nbytes = sum(host[ds].nbytes for ds in ids)
-        e2e = {"value": cu * args.steps * world / dt, "unit": UNIT,
+        nbytes = sum(host[ds].nbytes for ds in ids) * world
+        e2e = {"value": cu * args.steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": nbytes / args.steps,
                "d2h_bytes_per_step": (nbytes + 8 * args.steps * (1 if args.config != "c4" else 2)) / args.steps,
                "definition": "job = upload all fields (pinned) + K steps (per-step reduction read back) + "
@@ -405,14 +461,18 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic: seeded PCG64 fields with the BASELINE config shapes and value ranges",
-                "config": {"workload": WORKLOAD_TEXT[args.config], "mode": args.mode,
-                           "parallelism": "replicas" if world > 1 else "single GPU",
+                "config": {"workload": workload_text(args.config, world), "mode": args.mode,
+                           "parallelism": (f"{world} y-slabs of 4096^2 (domain 4096x{4096 * world}), one deep-halo "
+                                           "exchange per chain over NCCL" if sharded else
+                                           ("replicas" if world > 1 else "single GPU")),
                            "l2": "inputs exceed the 126 MB L2; no flush needed",
                            "effective_GBps": alg * args.steps * world / (ms / 1e3) / 1e9,
+                           "halo": {k: report.get(k) for k in ("halo_messages", "halo_bytes")} if sharded else None,
                            "untiled_value": untiled_value, "tiled_value": tiled_value,
+                           "windowed_value": windowed_value,
                            "speedup_vs_untiled": value / untiled_value if untiled_value else None,
                            "plan": {k: report.get(k) for k in ("executor", "tile_sizes", "cta_grid", "ctas",
-                                                                "max_skew",
+                                                                "max_skew", "grid_barriers",
                                                                 "subchains", "computed_points")}},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}

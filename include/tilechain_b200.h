@@ -62,8 +62,12 @@ enum {
 /* AccessMode (types.hpp:185) and ReduceOp (types.hpp:270) numbering. */
 enum { TCG_READ = 0, TCG_WRITE = 1, TCG_READ_WRITE = 2, TCG_INCREMENT = 3 };
 enum { TCG_RED_NONE = -1, TCG_RED_SUM = 0, TCG_RED_MIN = 1, TCG_RED_MAX = 2 };
-/* ExecMode kinds (runtime.hpp:25-35). */
-enum { TCG_UNTILED = 0, TCG_TILED = 1, TCG_TILED_AUTO = 2 };
+/* ExecMode kinds (runtime.hpp:25-35). TCG_TILED runs the reference tile
+ * plan (tile_sizes as in the reference, 0 = GPU sizer) on the L2-resident
+ * executor; TCG_WINDOWED selects the shared-memory windowed executor
+ * (tile_sizes = column block / stream tile bounds, 0 = sizer); TCG_TILED_AUTO
+ * times the executors per chain and keeps the fastest. */
+enum { TCG_UNTILED = 0, TCG_TILED = 1, TCG_TILED_AUTO = 2, TCG_WINDOWED = 3 };
 
 typedef struct tcg_runtime tcg_runtime;
 
@@ -92,7 +96,7 @@ int tcg_alloc_range(tcg_runtime* rt, int32_t ds, int64_t out[6]);
 int tcg_par_loop(tcg_runtime* rt, int32_t kernel_id, int32_t body, const int64_t range[6], int nargs,
                  const int32_t* args, int red_op, int nparams, const double* params, int32_t* out_handle);
 
-/* mode: TCG_UNTILED, TCG_TILED (tile_sizes used), TCG_TILED_AUTO. */
+/* mode: TCG_UNTILED, TCG_TILED / TCG_WINDOWED (tile_sizes used), TCG_TILED_AUTO. */
 int tcg_flush(tcg_runtime* rt, int mode, const int64_t tile_sizes[3]);
 int tcg_flush_default(tcg_runtime* rt);
 int tcg_set_default_mode(tcg_runtime* rt, int mode, const int64_t tile_sizes[3]);
@@ -106,6 +110,12 @@ int tcg_fill_logical(tcg_runtime* rt, int32_t ds, double v);
 int tcg_upload(tcg_runtime* rt, int32_t ds, const double* host);
 int tcg_download(tcg_runtime* rt, int32_t ds, double* host);
 int tcg_synchronize(tcg_runtime* rt);
+/* Box forms: host dense over box (inside the allocation); in a distributed
+ * runtime only the parts this process's ranks hold move. tcg_local_box: the
+ * part of the allocation this process holds (what it must upload). */
+int tcg_upload_box(tcg_runtime* rt, int32_t ds, const double* host, const int64_t box[6]);
+int tcg_download_box(tcg_runtime* rt, int32_t ds, double* host, const int64_t box[6]);
+int tcg_local_box(tcg_runtime* rt, int32_t ds, int64_t out[6]);
 
 /* Text outputs: write up to n bytes (NUL-terminated) and store the full
  * length + 1 in *needed. */

@@ -34,7 +34,7 @@ if DEBUG:
     NVCCFLAGS = NVCCFLAGS + ["-DTCG_DEBUG_PRINT"]
 
 HOST_SRCS = ["host/tcg_plan.cpp", "host/tcg_gpuplan.cpp", "host/tcg_dist.cpp", "host/tcg_runtime.cpp", "tcg_capi.cpp"]
-CUDA_SRCS = ["cuda/tcg_exec.cu", "cuda/tcg_comm.cu"]
+CUDA_SRCS = ["cuda/tcg_exec.cu", "cuda/tcg_tiled.cu", "cuda/tcg_l2.cu", "cuda/tcg_comm.cu"]
 
 
 def _headers() -> list[Path]:

@@ -29,6 +29,33 @@ def uniform(seed: int, shape, lo: float, hi: float) -> np.ndarray:
     return lo + (hi - lo) * g.random(shape)
 
 
+def uniform_box(seed: int, alloc: Range, box: Range, lo: float, hi: float) -> np.ndarray:
+    """The `box` part of uniform(seed, alloc.shape(), lo, hi) without drawing
+    the rest: the stream is in dim-0-fastest order over `alloc`, so whole
+    rows/planes of it are contiguous; the generator jumps to the box start
+    (one draw per double)."""
+    if box == alloc:
+        return uniform(seed, alloc.shape(), lo, hi)
+    dim = alloc.dim
+    for d in range(dim - 1):
+        if box.start(d) != alloc.start(d) or box.end(d) != alloc.end(d):
+            raise ValueError("uniform_box: box must span the allocation in all but the slowest dimension")
+    s = dim - 1
+    row = 1
+    for d in range(s):
+        row *= alloc.extent(d)
+    g = np.random.Generator(np.random.PCG64(seed))
+    g.bit_generator.advance((box.start(s) - alloc.start(s)) * row)
+    return lo + (hi - lo) * g.random(box.shape())
+
+
+def _upload_init(rt, ds, arr, box, alloc):
+    if box == alloc:
+        rt.upload(ds, arr)
+    else:
+        rt.upload_box(ds, arr, box)
+
+
 def _interior_mask(alloc: Range, box: Range) -> tuple:
     """numpy slices of `box` inside a dense array over `alloc` (dim 0 fastest)."""
     sl = []
@@ -200,19 +227,25 @@ class HydroC2:
 
     name = "c2_hydro2d"
 
-    def __init__(self, rt, n=4096, seed=7):
-        self.rt, self.n = rt, n
+    def __init__(self, rt, n=4096, seed=7, ny=None):
+        # ny > n: the weak-scaling domain n x (n * ranks), one n x n slab per
+        # rank; every rank draws only the rows it holds (uniform_box).
+        self.rt, self.n, self.ny = rt, n, ny or n
         self.st = {k: rt.declare_stencil(f"s{k}", pts) for k, pts in STENCILS_2D.items()}
         self.ident = self.st[0]
-        self.dom = Range.d2(0, n, 0, n)
+        self.dom = Range.d2(0, n, 0, self.ny)
         self.d = [rt.declare_field(f"d{i}", self.dom) for i in range(8)]
         al = rt.alloc_range(self.d[0])
-        self.init = {}
+        self.init, self.init_box = {}, {}
         for i, ds in enumerate(self.d):
-            self.init[ds] = uniform(seed * 1000 + i, al.shape(), 0.5, 1.5)
-            rt.upload(ds, self.init[ds])
+            box = rt.local_box(ds) if hasattr(rt, "local_box") else al
+            self.init[ds] = uniform_box(seed * 1000 + i, al, box, 0.5, 1.5)
+            self.init_box[ds] = box
+            _upload_init(rt, ds, self.init[ds], box, al)
 
     def loop_specs(self):
+        if getattr(self, "_specs", None) is not None:
+            return self._specs
         specs = []
         for k in range(12):
             kind = k % 5
@@ -222,6 +255,7 @@ class HydroC2:
                 args.append(ArgSpec(self.d[(k + 5) % 8], self.ident, R))
             args.append(ArgSpec(self.d[k % 8], self.ident, W))
             specs.append((KernelHandle(200 + k, f"hydro{k}", K.hydro_body(kind, r3)), args))
+        self._specs = specs
         return specs
 
     def enqueue_step(self) -> int:
@@ -232,14 +266,14 @@ class HydroC2:
                                  ArgSpec(self.d[5], self.ident, R)], ReduceOp.Min)
 
     def cell_updates_per_step(self):
-        return 13 * self.n * self.n
+        return 13 * self.n * self.ny
 
     def bytes_per_step(self):
         per_pt = 0
         for _, args in self.loop_specs():
             per_pt += 8 * len(args)
         per_pt += 3 * 8
-        return per_pt * self.n * self.n
+        return per_pt * self.n * self.ny
 
     def outputs(self):
         return {f"d{i}": self.rt.download(ds) for i, ds in enumerate(self.d)}

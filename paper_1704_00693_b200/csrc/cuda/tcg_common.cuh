@@ -1,0 +1,123 @@
+// Shared pieces of the CUDA executors (one copy per translation unit).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "../host/tcg_exec.hpp"
+#include "../kernels/tc_bodies.h"
+
+namespace tcg {
+
+namespace {
+
+#define TCG_CK(x)                                                                         \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kTiledThreads = 512;
+constexpr int kMaxParams = 16;
+
+__host__ __device__ __forceinline__ double red_identity(int op) {
+  return op == 0 ? 0.0 : (op == 1 ? HUGE_VAL : -HUGE_VAL);
+}
+__device__ __forceinline__ double red_combine(int op, double a, double b) {
+  return op == 0 ? a + b : (op == 1 ? (a < b ? a : b) : (a > b ? a : b));
+}
+
+// Block-wide reduction, deterministic for a fixed block shape: xor-shuffle
+// tree inside each warp, then warp results in warp order. Result on thread 0.
+__device__ double block_reduce(double v, int op) {
+  __shared__ double ws[32];
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nthr = blockDim.x * blockDim.y * blockDim.z;
+  for (int o = 16; o > 0; o >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((tid & 31) == 0) ws[tid >> 5] = v;
+  __syncthreads();
+  if (tid < 32) {
+    const int nw = (nthr + 31) >> 5;
+    v = tid < nw ? ws[tid] : red_identity(op);
+    for (int o = 16; o > 0; o >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(1024) k_fold(const double* __restrict__ p, int64_t n, int op, double* out) {
+  const int64_t chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int64_t a = static_cast<int64_t>(threadIdx.x) * chunk;
+  const int64_t b = a + chunk < n ? a + chunk : n;
+  double v = red_identity(op);
+  for (int64_t i = a; i < b; ++i) v = red_combine(op, v, p[i]);
+  v = block_reduce(v, op);
+  if (threadIdx.x == 0) *out = v;
+}
+
+// Uploads the chain tables into scratch; returns device pointers.
+struct ChainDev {
+  DevLoop* loops;
+  double* params;
+  DevStencils st;
+};
+
+template <class T>
+size_t align_up(size_t v) {
+  return (v + 255) / 256 * 256 + 0 * sizeof(T);
+}
+
+ChainDev upload_chain(const DevChain& ch, void* scratch, cudaStream_t st) {
+  const size_t nl = ch.loops.size() * sizeof(DevLoop);
+  const size_t np = std::max<size_t>(1, ch.params.size()) * sizeof(double);
+  const size_t ns = std::max<size_t>(1, ch.st_start.size()) * 4;
+  const size_t nq = std::max<size_t>(1, ch.st_pts.size()) * 4;
+  char* base = static_cast<char*>(scratch);
+  size_t off = 0;
+  ChainDev cd;
+  cd.loops = reinterpret_cast<DevLoop*>(base + off);
+  if (nl) TCG_CK(cudaMemcpyAsync(base + off, ch.loops.data(), nl, cudaMemcpyHostToDevice, st));
+  off += align_up<char>(nl);
+  cd.params = reinterpret_cast<double*>(base + off);
+  if (!ch.params.empty())
+    TCG_CK(cudaMemcpyAsync(base + off, ch.params.data(), ch.params.size() * 8, cudaMemcpyHostToDevice, st));
+  off += align_up<char>(np);
+  int32_t* s0 = reinterpret_cast<int32_t*>(base + off);
+  if (!ch.st_start.empty()) TCG_CK(cudaMemcpyAsync(s0, ch.st_start.data(), ch.st_start.size() * 4, cudaMemcpyHostToDevice, st));
+  off += align_up<char>(ns);
+  int32_t* s1 = reinterpret_cast<int32_t*>(base + off);
+  if (!ch.st_npts.empty()) TCG_CK(cudaMemcpyAsync(s1, ch.st_npts.data(), ch.st_npts.size() * 4, cudaMemcpyHostToDevice, st));
+  off += align_up<char>(ns);
+  int32_t* s2 = reinterpret_cast<int32_t*>(base + off);
+  if (!ch.st_pts.empty()) TCG_CK(cudaMemcpyAsync(s2, ch.st_pts.data(), ch.st_pts.size() * 4, cudaMemcpyHostToDevice, st));
+  cd.st = DevStencils{s0, s1, s2};
+  return cd;
+}
+
+size_t chain_bytes(const DevChain& ch) {
+  return align_up<char>(ch.loops.size() * sizeof(DevLoop)) + align_up<char>(std::max<size_t>(1, ch.params.size()) * 8) +
+         2 * align_up<char>(std::max<size_t>(1, ch.st_start.size()) * 4) +
+         align_up<char>(std::max<size_t>(1, ch.st_pts.size()) * 4) + 256;
+}
+}  // namespace
+
+struct DeviceExec::Buf {
+  Range alloc;
+  int64_t x0 = 0, nxp = 0, py = 0, pz = 0, ny = 1, nz = 1;
+  double* mem[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+  int cur = 0;
+};
+
+struct DeviceExec::PlanBufs {
+  void* mem = nullptr;
+  DevCta* ctas = nullptr;
+  int32_t* boxes = nullptr;
+  int32_t* win = nullptr;
+  int32_t* wboxes = nullptr;
+};
+
+}  // namespace tcg

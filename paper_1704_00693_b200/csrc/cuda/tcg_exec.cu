@@ -16,61 +16,11 @@
 //                    order, executor.cpp:175-176).
 // All arithmetic is fp64 and compiled with -fmad=false so every per-point
 // expression rounds exactly like the reference's (FMA-free) host build.
-#include <cuda_runtime.h>
-
-#include <cmath>
-#include <cstring>
-
-#include "../host/tcg_exec.hpp"
-#include "../kernels/tc_bodies.h"
+#include "tcg_common.cuh"
 
 namespace tcg {
 
 namespace {
-
-#define TCG_CK(x)                                                                         \
-  do {                                                                                    \
-    cudaError_t e_ = (x);                                                                 \
-    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-constexpr int kTiledThreads = 512;
-constexpr int kMaxParams = 16;
-
-__host__ __device__ __forceinline__ double red_identity(int op) {
-  return op == 0 ? 0.0 : (op == 1 ? HUGE_VAL : -HUGE_VAL);
-}
-__device__ __forceinline__ double red_combine(int op, double a, double b) {
-  return op == 0 ? a + b : (op == 1 ? (a < b ? a : b) : (a > b ? a : b));
-}
-
-// Block-wide reduction, deterministic for a fixed block shape: xor-shuffle
-// tree inside each warp, then warp results in warp order. Result on thread 0.
-__device__ double block_reduce(double v, int op) {
-  __shared__ double ws[32];
-  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-  const int nthr = blockDim.x * blockDim.y * blockDim.z;
-  for (int o = 16; o > 0; o >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, o));
-  __syncthreads();
-  if ((tid & 31) == 0) ws[tid >> 5] = v;
-  __syncthreads();
-  if (tid < 32) {
-    const int nw = (nthr + 31) >> 5;
-    v = tid < nw ? ws[tid] : red_identity(op);
-    for (int o = 16; o > 0; o >>= 1) v = red_combine(op, v, __shfl_xor_sync(0xffffffffu, v, o));
-  }
-  return v;
-}
-
-__global__ void __launch_bounds__(1024) k_fold(const double* __restrict__ p, int64_t n, int op, double* out) {
-  const int64_t chunk = (n + blockDim.x - 1) / blockDim.x;
-  const int64_t a = static_cast<int64_t>(threadIdx.x) * chunk;
-  const int64_t b = a + chunk < n ? a + chunk : n;
-  double v = red_identity(op);
-  for (int64_t i = a; i < b; ++i) v = red_combine(op, v, p[i]);
-  v = block_reduce(v, op);
-  if (threadIdx.x == 0) *out = v;
-}
 
 // ---------------------------------------------------------------------------
 // Untiled per-loop executor.
@@ -140,10 +90,10 @@ struct GAcc {
   __device__ __forceinline__ bool reduces() const { return L.has_red != 0; }
 };
 
-// Rows (2D: y, 3D: z) walked by one thread of the untiled executor.
-constexpr int kUntiledRun = 4;
+// Rows (2D: y, 3D: z) walked by one thread of the untiled executor
+// (template parameter kUntiledRun of k_untiled; 4 unless tuned).
 
-template <int DIM, int BODY>
+template <int DIM, int BODY, int kUntiledRun = 4>
 __global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch L) {
   GAcc acc{L, {}, 0, 0, 0, red_identity(L.red_op)};
   if (DIM == 1) {
@@ -198,49 +148,11 @@ __global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch
   }
 }
 
-// ---------------------------------------------------------------------------
-// Windowed tiled executor.
-#include "tcg_tiled.cuh"
-
-
-// Launch of k_tiled<DIM, NT>: NT = 512 / (CTAs per SM) threads.
-template <int DIM, int NT>
-void launch_tiled_nt(const DevTiledPlan& P, int64_t smem, cudaStream_t st) {
-  TCG_CK(cudaFuncSetAttribute(tiled::k_tiled<DIM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(smem)));
-  tiled::k_tiled<DIM, NT><<<dim3(static_cast<unsigned>(P.nctas)), dim3(NT), smem, st>>>(P);
-}
-
-template <int DIM>
-void launch_tiled(const DevTiledPlan& P, int threads, int64_t smem, cudaStream_t st) {
-  if (threads == 512)
-    launch_tiled_nt<DIM, 512>(P, smem, st);
-  else if (threads == 256)
-    launch_tiled_nt<DIM, 256>(P, smem, st);
-  else
-    launch_tiled_nt<DIM, 128>(P, smem, st);
-}
-
 }  // namespace
+
 
 // ---------------------------------------------------------------------------
 // Host side.
-
-struct DeviceExec::Buf {
-  Range alloc;
-  int64_t x0 = 0, nxp = 0, py = 0, pz = 0, ny = 1, nz = 1;
-  double* mem[2] = {nullptr, nullptr};
-  size_t bytes = 0;
-  int cur = 0;
-};
-
-struct DeviceExec::PlanBufs {
-  void* mem = nullptr;
-  DevCta* ctas = nullptr;
-  int32_t* boxes = nullptr;
-  int32_t* win = nullptr;
-  int32_t* wboxes = nullptr;
-};
 
 void select_device(int device) {
   int ndev = 0;
@@ -278,6 +190,11 @@ DeviceExec::~DeviceExec() {
   for (auto& pb : plan_cache_) {
     cudaFree(pb.second->mem);
     delete pb.second;
+  }
+  for (auto& ic : item_cache_) {
+    cudaFree(ic.items);
+    cudaFree(ic.deps);
+    cudaFree(ic.flags);
   }
   if (scratch_) cudaFree(scratch_);
   if (partials_) cudaFree(partials_);
@@ -497,6 +414,8 @@ bool DeviceExec::elapsed_ms(void* a, void* b, float* ms) {
 
 void DeviceExec::release(void* ev) { ev_pool_.push_back(ev); }
 
+void DeviceExec::wait_event(void* ev) { TCG_CK(cudaEventSynchronize(static_cast<cudaEvent_t>(ev))); }
+
 void DeviceExec::set_timing(bool on) {
   timing_ = on;
   double a, b;
@@ -547,64 +466,6 @@ double* DeviceExec::ensure_partials(size_t n) {
   return partials_;
 }
 
-int64_t DeviceExec::window_budget_doubles(int nloops, int nred, int ctas_per_sm) const {
-  const int k = std::max(1, ctas_per_sm);
-  const int threads = kTiledThreads / k;
-  // Per-CTA share of the SM (1 KB of every CTA's share is reserved by the driver).
-  const int64_t per_block = std::min<int64_t>(info_.smem_optin, info_.smem_per_sm / k - 1024);
-  const int64_t fixed = static_cast<int64_t>(sizeof(tiled::Shared)) + 512 + 256 +
-                        static_cast<int64_t>(nloops) * (kMaxArgs * 16 + 6 * 4 + static_cast<int64_t>(sizeof(DevLoop))) +
-                        static_cast<int64_t>(nred) * threads * 8;
-  return std::max<int64_t>(0, (per_block - fixed) / 8);
-}
-
-namespace {
-// Uploads the chain tables into scratch; returns device pointers.
-struct ChainDev {
-  DevLoop* loops;
-  double* params;
-  DevStencils st;
-};
-
-template <class T>
-size_t align_up(size_t v) {
-  return (v + 255) / 256 * 256 + 0 * sizeof(T);
-}
-
-ChainDev upload_chain(const DevChain& ch, void* scratch, cudaStream_t st) {
-  const size_t nl = ch.loops.size() * sizeof(DevLoop);
-  const size_t np = std::max<size_t>(1, ch.params.size()) * sizeof(double);
-  const size_t ns = std::max<size_t>(1, ch.st_start.size()) * 4;
-  const size_t nq = std::max<size_t>(1, ch.st_pts.size()) * 4;
-  char* base = static_cast<char*>(scratch);
-  size_t off = 0;
-  ChainDev cd;
-  cd.loops = reinterpret_cast<DevLoop*>(base + off);
-  if (nl) TCG_CK(cudaMemcpyAsync(base + off, ch.loops.data(), nl, cudaMemcpyHostToDevice, st));
-  off += align_up<char>(nl);
-  cd.params = reinterpret_cast<double*>(base + off);
-  if (!ch.params.empty())
-    TCG_CK(cudaMemcpyAsync(base + off, ch.params.data(), ch.params.size() * 8, cudaMemcpyHostToDevice, st));
-  off += align_up<char>(np);
-  int32_t* s0 = reinterpret_cast<int32_t*>(base + off);
-  if (!ch.st_start.empty()) TCG_CK(cudaMemcpyAsync(s0, ch.st_start.data(), ch.st_start.size() * 4, cudaMemcpyHostToDevice, st));
-  off += align_up<char>(ns);
-  int32_t* s1 = reinterpret_cast<int32_t*>(base + off);
-  if (!ch.st_npts.empty()) TCG_CK(cudaMemcpyAsync(s1, ch.st_npts.data(), ch.st_npts.size() * 4, cudaMemcpyHostToDevice, st));
-  off += align_up<char>(ns);
-  int32_t* s2 = reinterpret_cast<int32_t*>(base + off);
-  if (!ch.st_pts.empty()) TCG_CK(cudaMemcpyAsync(s2, ch.st_pts.data(), ch.st_pts.size() * 4, cudaMemcpyHostToDevice, st));
-  cd.st = DevStencils{s0, s1, s2};
-  return cd;
-}
-
-size_t chain_bytes(const DevChain& ch) {
-  return align_up<char>(ch.loops.size() * sizeof(DevLoop)) + align_up<char>(std::max<size_t>(1, ch.params.size()) * 8) +
-         2 * align_up<char>(std::max<size_t>(1, ch.st_start.size()) * 4) +
-         align_up<char>(std::max<size_t>(1, ch.st_pts.size()) * 4) + 256;
-}
-}  // namespace
-
 void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   void* scratch = ensure_scratch(chain_bytes(ch));
@@ -636,15 +497,36 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
     }
     L.st = cd.st;
     dim3 block, grid;
+    // Block shape and rows per thread (2D): TCG_UNTILED_CFG="bx,by,run"
+    // overrides the default 32x8x4 (tuning experiments).
+    static const int3 ucfg = [] {
+      // Measured on B200 (c2 4096^2, tools/sweep_untiled.sh): 256x1x4 best.
+      int3 c{256, 1, 4};
+      if (const char* e = std::getenv("TCG_UNTILED_CFG")) std::sscanf(e, "%d,%d,%d", &c.x, &c.y, &c.z);
+      if (c.x * c.y > 256 || c.x * c.y < 32 || (c.z != 2 && c.z != 4 && c.z != 8)) c = int3{256, 1, 4};
+      return c;
+    }();
+    static const int3 ucfg3 = [] {
+      // Measured on B200 (c3 512^3, tools/sweep3.sh): 64x2 with 8 planes per thread.
+      int3 c{64, 2, 8};
+      if (const char* e = std::getenv("TCG_UNTILED_CFG3")) std::sscanf(e, "%d,%d,%d", &c.x, &c.y, &c.z);
+      if (c.x * c.y > 256 || c.x * c.y < 32 || (c.z != 4 && c.z != 8)) c = int3{64, 2, 8};
+      return c;
+    }();
+    const int run2 = ch.dim == 2 ? ucfg.z : ch.dim == 3 ? ucfg3.z : 4;
     if (ch.dim == 1) {
       block = dim3(256, 1, 1);
       grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + 255) / 256)), 1, 1);
+    } else if (ch.dim == 2) {
+      block = dim3(static_cast<unsigned>(ucfg.x), static_cast<unsigned>(ucfg.y), 1);
+      const int64_t ry = static_cast<int64_t>(ucfg.y) * run2;  // rows of y per block
+      grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + ucfg.x - 1) / ucfg.x)),
+                  static_cast<unsigned>(std::max<int64_t>(1, (n[1] + ry - 1) / ry)), 1);
     } else {
-      block = dim3(32, 8, 1);
-      const int64_t ry = ch.dim == 2 ? 8 * kUntiledRun : 8;  // rows of y per block
-      grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + 31) / 32)),
-                  static_cast<unsigned>(std::max<int64_t>(1, (n[1] + ry - 1) / ry)),
-                  static_cast<unsigned>(ch.dim == 3 ? std::max<int64_t>(1, (n[2] + kUntiledRun - 1) / kUntiledRun) : 1));
+      block = dim3(static_cast<unsigned>(ucfg3.x), static_cast<unsigned>(ucfg3.y), 1);
+      grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + ucfg3.x - 1) / ucfg3.x)),
+                  static_cast<unsigned>(std::max<int64_t>(1, (n[1] + ucfg3.y - 1) / ucfg3.y)),
+                  static_cast<unsigned>(std::max<int64_t>(1, (n[2] + run2 - 1) / run2)));
     }
     const int64_t nblocks = static_cast<int64_t>(grid.x) * grid.y * grid.z;
     if (L.has_red) L.partials = ensure_partials(static_cast<size_t>(nblocks));
@@ -668,8 +550,14 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
       constexpr int B = decltype(tag)::value;
       if (ch.dim == 1)
         k_untiled<1, B><<<grid, block, 0, st>>>(L);
+      else if (ch.dim == 2 && run2 == 2)
+        k_untiled<2, B, 2><<<grid, block, 0, st>>>(L);
+      else if (ch.dim == 2 && run2 == 8)
+        k_untiled<2, B, 8><<<grid, block, 0, st>>>(L);
       else if (ch.dim == 2)
         k_untiled<2, B><<<grid, block, 0, st>>>(L);
+      else if (run2 == 8)
+        k_untiled<3, B, 8><<<grid, block, 0, st>>>(L);
       else
         k_untiled<3, B><<<grid, block, 0, st>>>(L);
     });
@@ -689,104 +577,6 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
   }
   if (ch.nred > 0) {
     TCG_CK(cudaMemcpyAsync(red_out, red_dev_, sizeof(double) * static_cast<size_t>(ch.nred), cudaMemcpyDeviceToHost, st));
-    TCG_CK(cudaStreamSynchronize(st));
-  }
-}
-
-DeviceExec::PlanBufs* DeviceExec::plan_bufs(const GpuTiledPlan& gp, uint64_t key) {
-  for (auto& pb : plan_cache_)
-    if (pb.first == key) return pb.second;
-  cudaStream_t st = static_cast<cudaStream_t>(stream_);
-  auto* pb = new PlanBufs;
-  const size_t a = align_up<char>(gp.ctas.size() * sizeof(DevCta));
-  const size_t b = align_up<char>(std::max<size_t>(1, gp.boxes.size()) * 4);
-  const size_t c = align_up<char>(std::max<size_t>(1, gp.win.size()) * 4);
-  const size_t d = align_up<char>(std::max<size_t>(1, gp.wboxes.size()) * 4);
-  TCG_CK(cudaMalloc(&pb->mem, a + b + c + d));
-  char* m = static_cast<char*>(pb->mem);
-  pb->ctas = reinterpret_cast<DevCta*>(m);
-  pb->boxes = reinterpret_cast<int32_t*>(m + a);
-  pb->win = reinterpret_cast<int32_t*>(m + a + b);
-  pb->wboxes = reinterpret_cast<int32_t*>(m + a + b + c);
-  TCG_CK(cudaMemcpyAsync(pb->ctas, gp.ctas.data(), gp.ctas.size() * sizeof(DevCta), cudaMemcpyHostToDevice, st));
-  if (!gp.boxes.empty()) TCG_CK(cudaMemcpyAsync(pb->boxes, gp.boxes.data(), gp.boxes.size() * 4, cudaMemcpyHostToDevice, st));
-  if (!gp.win.empty()) TCG_CK(cudaMemcpyAsync(pb->win, gp.win.data(), gp.win.size() * 4, cudaMemcpyHostToDevice, st));
-  if (!gp.wboxes.empty())
-    TCG_CK(cudaMemcpyAsync(pb->wboxes, gp.wboxes.data(), gp.wboxes.size() * 4, cudaMemcpyHostToDevice, st));
-  TCG_CK(cudaStreamSynchronize(st));
-  plan_cache_.emplace_back(key, pb);
-  if (plan_cache_.size() > 64) {
-    cudaFree(plan_cache_.front().second->mem);
-    delete plan_cache_.front().second;
-    plan_cache_.erase(plan_cache_.begin());
-  }
-  return pb;
-}
-
-void DeviceExec::run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t key, double* red_out) {
-  cudaStream_t st = static_cast<cudaStream_t>(stream_);
-  PlanBufs* pb = plan_bufs(gp, key);
-  void* scratch = ensure_scratch(chain_bytes(ch));
-  const ChainDev cd = upload_chain(ch, scratch, st);
-  DevTiledPlan P{};
-  P.dim = gp.dim;
-  P.nloops = gp.nloops;
-  P.ndat = gp.ndat;
-  P.nred = gp.nred;
-  P.nctas = static_cast<int32_t>(gp.ctas.size());
-  P.smem_doubles = static_cast<int32_t>((gp.smem_doubles + 1) / 2 * 2);
-  P.prefetch = gp.prefetch ? 1 : 0;
-  P.ctas = pb->ctas;
-  P.boxes = pb->boxes;
-  P.win = pb->win;
-  P.wboxes = pb->wboxes;
-  P.loops = cd.loops;
-  P.params = cd.params;
-  P.stencils = cd.st;
-  // Device fields come from the lowered chain (the target's field map: the
-  // undistributed fields or one rank's); the plan only knows chain slots.
-  if (ch.dat_ids.size() != static_cast<size_t>(gp.ndat))
-    throw PlanError("tiled executor: chain and plan disagree on the dataset count");
-  for (int k = 0; k < gp.ndat; ++k) {
-    P.dats[k] = gp.dats[static_cast<size_t>(k)];
-    const int f = ch.dat_ids[static_cast<size_t>(k)];
-    P.src[k] = view(f, false);
-    P.dst[k] = gp.dats[static_cast<size_t>(k)].pingpong ? view(f, true) : P.src[k];
-  }
-  for (int r = 0; r < gp.nred && r < kMaxRed; ++r) P.red_op[r] = ch.red_op[static_cast<size_t>(r)];
-  if (gp.nred > 0) P.red_partials = ensure_partials(static_cast<size_t>(gp.nred) * gp.ctas.size());
-  P.red_out = red_dev_;
-  const int64_t smem = static_cast<int64_t>(P.smem_doubles) * 8 +
-                       static_cast<int64_t>(gp.nloops) * (sizeof(DevLoop) + kMaxArgs * 16 + 6 * 4) +
-                       static_cast<int64_t>(gp.nred) * gp.threads * 8;
-  if (smem > info_.smem_optin) throw PlanError("tiled executor: shared memory request exceeds the device limit");
-  void* e0 = nullptr;
-  if (timing_) {
-    e0 = take_event();
-    TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e0), st));
-  }
-  if (gp.dim == 1)
-    launch_tiled<1>(P, gp.threads, smem, st);
-  else if (gp.dim == 2)
-    launch_tiled<2>(P, gp.threads, smem, st);
-  else
-    launch_tiled<3>(P, gp.threads, smem, st);
-  TCG_CK(cudaGetLastError());
-  if (timing_) {
-    void* e1 = take_event();
-    TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e1), st));
-    ev_tiled_.emplace_back(e0, e1);
-  }
-  ++launches_;
-  for (int k = 0; k < gp.ndat; ++k)
-    if (gp.dats[static_cast<size_t>(k)].pingpong) swap(ch.dat_ids[static_cast<size_t>(k)]);
-  for (int r = 0; r < gp.nred; ++r) {
-    k_fold<<<1, 1024, 0, st>>>(P.red_partials + static_cast<int64_t>(r) * P.nctas, P.nctas, P.red_op[r], red_dev_ + r);
-    TCG_CK(cudaGetLastError());
-    ++launches_;
-  }
-  if (gp.nred > 0) {
-    TCG_CK(cudaMemcpyAsync(red_out, red_dev_, sizeof(double) * static_cast<size_t>(gp.nred), cudaMemcpyDeviceToHost, st));
     TCG_CK(cudaStreamSynchronize(st));
   }
 }

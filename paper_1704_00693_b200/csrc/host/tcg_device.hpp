@@ -42,6 +42,19 @@ struct DevLoop {
   DevArg args[kMaxArgs];
 };
 
+// One (tile, loop) work item of the L2-resident tiled executor: the loop's
+// range inside the tile (TilingPlan::range(t, l), planner.cpp:158-201).
+struct DevItem {
+  int32_t loop;
+  int32_t sync;        // 1: grid barrier after this item (barrier mode)
+  int32_t lo[3], hi[3];
+  int32_t cx, cy, nch; // chunk grid of the item (x chunks, y chunks, total)
+  int32_t flag_off;    // dataflow mode: first completion flag of this item's chunks
+  int32_t dep_off;     // dataflow mode: deps[dep_off, dep_off + ndeps) = earlier items it conflicts with
+  int32_t ndeps;
+  int32_t pad[2];
+};
+
 // Stencil table: points of stencil s are pts[3*start[s] ..].
 struct DevStencils {
   const int32_t* start;

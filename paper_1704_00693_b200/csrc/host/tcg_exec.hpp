@@ -1,6 +1,7 @@
 // Host-side interface of the CUDA executors (implemented in
 // csrc/cuda/tcg_exec.cu). Host code includes this without CUDA headers.
 #pragma once
+#include <array>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -85,6 +86,15 @@ class DeviceExec {
   void run_untiled(const DevChain& ch, double* red_out);
   // Execute with the windowed tiled executor.
   void run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t plan_key, double* red_out);
+  // Execute a reference tile plan (the (tile, loop) items in order, as
+  // execute_plan does, executor.cpp:209-250) in one persistent cooperative
+  // launch: every CTA works on each item, a grid barrier separates items, so
+  // a tile's data stays in the 126 MB L2 from loop to loop.
+  // Dataflow mode (deps non-empty): no grid barriers; a CTA waits, chunk by
+  // chunk, for the chunks of the conflicting earlier items within `reach` of
+  // its chunk (completion flags in global memory).
+  void run_l2(const DevChain& ch, const std::vector<DevItem>& items, const std::vector<int32_t>& deps,
+              const std::array<int32_t, 3>& reach, uint64_t plan_key, double* red_out);
 
   void synchronize();
   void* stream() const { return stream_; }
@@ -97,6 +107,7 @@ class DeviceExec {
   // an event recorded on the stream; elapsed_ms(a, b) is valid once b completed.
   void* record();
   bool elapsed_ms(void* a, void* b, float* ms);
+  void wait_event(void* ev);
   void release(void* ev);
   void kernel_ms(double* tiled_ms, int64_t* tiled_n, double* untiled_ms, int64_t* untiled_n);
   // Bytes of dynamic shared memory available for windows for a chain shape.
@@ -119,9 +130,18 @@ class DeviceExec {
   double* redbuf_ = nullptr;
   size_t redbuf_n_ = 0;
   std::vector<std::pair<uint64_t, PlanBufs*>> plan_cache_;
+  struct ItemBufs {
+    uint64_t key = 0;
+    size_t nitems = 0;
+    DevItem* items = nullptr;
+    int32_t* deps = nullptr;
+    uint32_t* flags = nullptr;
+  };
+  std::vector<ItemBufs> item_cache_;
+  uint32_t epoch_ = 0;
   int64_t launches_ = 0;
   bool timing_ = false;
-  std::vector<std::pair<void*, void*>> ev_tiled_, ev_untiled_;  // (start, stop) event pairs
+  std::vector<std::pair<void*, void*>> ev_tiled_, ev_untiled_;  // (start, stop) event pairs (k_l2tiled counts as tiled)
   std::vector<void*> ev_pool_;
   void* take_event();
   void* ensure_scratch(size_t bytes);

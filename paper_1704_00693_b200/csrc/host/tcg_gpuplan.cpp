@@ -352,8 +352,10 @@ GpuTiledPlan build_gpu_tiled_plan(const LoopChain& chain, const std::vector<Fiel
       by_list = pick(choice.block[1], {32, 16, 8, 4});
       st_list = pick(choice.stream_tile, {4, 2, 1});
     }
-    const std::vector<int> k_list = choice.ctas_per_sm > 0 ? std::vector<int>{choice.ctas_per_sm}
-                                                           : std::vector<int>{2, 1, 4};
+    // 1 or 2 CTAs per SM (512 / 256 threads; the kernels built).
+    const std::vector<int> k_list = choice.ctas_per_sm == 1 || choice.ctas_per_sm == 2
+                                        ? std::vector<int>{choice.ctas_per_sm}
+                                        : std::vector<int>{2, 1};
     for (int k : k_list)
     for (int64_t st : st_list)
       for (int64_t bx : bx_list)

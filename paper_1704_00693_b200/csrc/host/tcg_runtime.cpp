@@ -1,7 +1,9 @@
 #include "tcg_runtime.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <limits>
 
 #include "../kernels/tc_bodies.h"
 
@@ -19,6 +21,12 @@ double secs_since(std::chrono::steady_clock::time_point t0) {
 struct WindowOverflow : PlanError {
   explicit WindowOverflow(const std::string& m) : PlanError(m) {}
 };
+
+int64_t chain_points(const LoopChain& c) {
+  int64_t n = 0;
+  for (const LoopRecord& lp : c.loops) n += lp.range.volume();
+  return n;
+}
 
 LoopChain slice(const LoopChain& c, size_t a, size_t b) {
   LoopChain s;
@@ -66,6 +74,7 @@ std::string ExecutionReport::to_text() const {
     kv("ctas", std::to_string(ctas));
     kv("subchains", std::to_string(subchains));
     kv("computed_points", std::to_string(computed_points));
+    if (executor == "tiled") kv("grid_barriers", std::to_string(l2_syncs));
   }
   kv("tiles", std::to_string(tiles_executed));
   kv("loops", std::to_string(loops.size()));
@@ -97,24 +106,33 @@ Runtime::Runtime(int dim, RuntimeConfig cfg) : dim_(dim), cfg_(cfg) {
   if (cfg_.threads < 1) throw InvalidArgument("Runtime: threads must be >= 1");
   if (cfg_.skew_allowance < 0) throw InvalidArgument("Runtime: skew_allowance must be >= 0");
   // tiled_auto decisions persisted across processes (like a library autotune
-  // cache): "signature tiled_ms untiled_ms tiled_fits" per line.
+  // cache): "signature ms_l2 ms_untiled ms_windowed fits_mask" per line.
   if (const char* path = std::getenv("TCG_AUTOTUNE_FILE")) {
     autotune_file_ = path;
     if (FILE* f = std::fopen(path, "r")) {
       unsigned long long sig = 0;
-      float tm = 0, um = 0;
+      float m0 = 0, m1 = 0, m2 = 0;
       int fits = 0;
-      while (std::fscanf(f, "%llx %f %f %d", &sig, &tm, &um, &fits) == 4) {
+      while (std::fscanf(f, "%llx %f %f %f %d", &sig, &m0, &m1, &m2, &fits) == 5) {
         AutoStat& a = auto_[static_cast<uint64_t>(sig)];
-        a.tiled_runs = a.untiled_runs = 2;
-        a.tiled_ms = tm;
-        a.untiled_ms = um;
-        a.tiled_fits = fits != 0;
+        const float m[kCand] = {m0, m1, m2};
+        for (int c = 0; c < kCand; ++c) {
+          a.runs[c] = 2;
+          a.ms[c] = m[c];
+          a.fits[c] = ((fits >> c) & 1) != 0;
+        }
         a.saved = true;
       }
       std::fclose(f);
     }
   }
+}
+
+int Runtime::AutoStat::best() const {
+  int b = 1;  // untiled always runs
+  for (int c = 0; c < kCand; ++c)
+    if (fits[c] && ms[c] < ms[b]) b = c;
+  return b;
 }
 
 Runtime::~Runtime() = default;
@@ -317,7 +335,7 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
   DeviceExec& dev = device();
   const int s = chain.dim - 1;
   GpuTileChoice choice;
-  if (mode.kind == ExecMode::Kind::Tiled) {
+  if (mode.kind == ExecMode::Kind::Windowed) {
     // Explicit sizes are upper bounds; 0 leaves that dimension to the sizer.
     for (int d = 0; d < chain.dim; ++d) {
       if (mode.tile_sizes[d] <= 0) continue;
@@ -413,6 +431,272 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
   }
 }
 
+namespace {
+// Access footprint of one (tile, loop) item: per dataset, the box it reads
+// (range dilated by the read stencil) and the box it writes.
+struct Footprint {
+  std::vector<std::pair<DatasetId, Range>> reads, writes;
+};
+Footprint footprint(const LoopChain& chain, const LoopRecord& lp, const Range& r) {
+  Footprint f;
+  for (const ArgSpec& a : lp.args) {
+    if (mode_reads(a.mode)) {
+      const Stencil& st = chain.stencil(a.stencil);
+      Point lo{0, 0, 0}, hi{0, 0, 0};
+      for (int d = 0; d < chain.dim; ++d) {
+        lo[d] = std::min<int64_t>(st.min_offset(d), 0);
+        hi[d] = std::max<int64_t>(st.max_offset(d), 0);
+      }
+      f.reads.emplace_back(a.dataset, r.dilated(lo, hi));
+    }
+    if (mode_writes(a.mode)) f.writes.emplace_back(a.dataset, r);
+  }
+  return f;
+}
+bool overlaps(const std::vector<std::pair<DatasetId, Range>>& a, const std::vector<std::pair<DatasetId, Range>>& b) {
+  for (const auto& [da, ra] : a)
+    for (const auto& [db, rb] : b)
+      if (da == db && !ra.intersect(rb).empty()) return true;
+  return false;
+}
+}  // namespace
+
+// GPU sizer of the L2 executor. Only the slowest dimension is tiled. A tile
+// of sub-chain [b, e) touches (ts + skew + 2) slowest-dim slices of every
+// dataset of the sub-chain; that must stay within the L2 budget. Sub-chain
+// boundaries come from a cost model minimised over all split points:
+//   cost(b, e) = DRAM bytes(b, e) / BW + items(b, e) * c_item,
+// DRAM bytes = one read of every dataset the sub-chain reads and one write
+// of every dataset it writes (the L2 holds the rest), items = tiles * loops
+// (each item ends in a grid barrier at worst).
+namespace {
+struct SubInfo {
+  int64_t slice = 0;  // bytes of one slowest-dim slice over the sub-chain's datasets
+  int64_t skew = 0;   // sum of slowest-dim read reaches (upper bound of the plan skew)
+  int64_t dram = 0;   // compulsory DRAM bytes
+  int64_t extent = 1; // slowest-dim extent of the sub-chain's union
+};
+}  // namespace
+
+std::vector<Runtime::L2Sub> Runtime::l2_split(const LoopChain& chain, const Target& t) const {
+  const int s = chain.dim - 1;
+  const int L = static_cast<int>(chain.size());
+  int64_t budget = (device_ready() ? dev_->info().l2_bytes : int64_t{126} << 20) * 70 / 100;
+  if (const char* e = std::getenv("TCG_L2_BUDGET_MB")) budget = std::atoll(e) << 20;
+  double c_item = 3e-6, bw = 6.0e12;
+  if (const char* e = std::getenv("TCG_L2_ITEM_US")) c_item = std::atof(e) * 1e-6;
+  auto info = [&](int b, int e) {
+    SubInfo si;
+    std::map<DatasetId, int> use;  // bit 1 read, bit 2 written
+    int64_t lo = std::numeric_limits<int64_t>::max(), hi = std::numeric_limits<int64_t>::min();
+    for (int l = b; l < e; ++l) {
+      const LoopRecord& lp = chain.loops[static_cast<size_t>(l)];
+      int64_t reach = 0;
+      for (const ArgSpec& a : lp.args) {
+        use[a.dataset] |= (mode_reads(a.mode) ? 1 : 0) | (mode_writes(a.mode) ? 2 : 0);
+        if (mode_reads(a.mode)) {
+          const Stencil& st = chain.stencil(a.stencil);
+          reach = std::max<int64_t>({reach, static_cast<int64_t>(std::llabs(st.min_offset(s))),
+                                     static_cast<int64_t>(std::llabs(st.max_offset(s)))});
+        }
+      }
+      si.skew += reach;
+      lo = std::min(lo, lp.range.start(s));
+      hi = std::max(hi, lp.range.end(s));
+    }
+    si.extent = std::max<int64_t>(1, hi - lo);
+    for (const auto& [ds, u] : use) {
+      const Range& al = t.alloc[static_cast<size_t>(ds)];
+      int64_t b8 = 8;
+      for (int d = 0; d < s; ++d) b8 *= al.extent(d);
+      si.slice += b8;
+      const int64_t field = b8 * al.extent(s);
+      si.dram += ((u & 1) ? field : 0) + ((u & 2) ? field : 0);
+    }
+    return si;
+  };
+  // ts(b, e): deepest tile whose working set fits; a single loop needs no
+  // reuse and runs as one item.
+  auto tile_of = [&](int b, int e, const SubInfo& si) -> int64_t {
+    if (e - b == 1) return si.extent;
+    const int64_t rows = budget / std::max<int64_t>(1, si.slice);
+    return rows - si.skew - 2;
+  };
+  std::vector<double> best(static_cast<size_t>(L) + 1, 1e300);
+  std::vector<int> from(static_cast<size_t>(L) + 1, -1);
+  std::vector<int64_t> tsb(static_cast<size_t>(L) + 1, 1);
+  best[0] = 0;
+  constexpr int kMaxSub = 32;  // loops per launch (descriptors in kernel parameters)
+  for (int e = 1; e <= L; ++e)
+    for (int b = e - 1; b >= std::max(0, e - kMaxSub); --b) {
+      const SubInfo si = info(b, e);
+      const int64_t ts = tile_of(b, e, si);
+      if (ts < 1) break;  // longer sub-chains only get worse
+      const double items = static_cast<double>((si.extent + ts - 1) / ts) * (e - b);
+      const double c = best[static_cast<size_t>(b)] + static_cast<double>(si.dram) / bw + items * c_item;
+      if (c < best[static_cast<size_t>(e)]) {
+        best[static_cast<size_t>(e)] = c;
+        from[static_cast<size_t>(e)] = b;
+        tsb[static_cast<size_t>(e)] = ts;
+      }
+    }
+  std::vector<L2Sub> subs;
+  for (int e = L; e > 0; e = from[static_cast<size_t>(e)]) {
+    if (from[static_cast<size_t>(e)] < 0) {  // a single loop that cannot fit: one item
+      subs.push_back(L2Sub{static_cast<size_t>(e - 1), static_cast<size_t>(e), int64_t{1} << 40});
+      from[static_cast<size_t>(e)] = e - 1;
+      continue;
+    }
+    subs.push_back(L2Sub{static_cast<size_t>(from[static_cast<size_t>(e)]), static_cast<size_t>(e),
+                         tsb[static_cast<size_t>(e)]});
+  }
+  std::reverse(subs.begin(), subs.end());
+  if (const char* e = std::getenv("TCG_L2_TS")) {  // tuning: fixed depth, <= 32 loops per sub-chain
+    subs.clear();
+    for (size_t b = 0; b < chain.size(); b += 32)
+      subs.push_back(L2Sub{b, std::min(chain.size(), b + 32), std::max<int64_t>(1, std::atoll(e))});
+  }
+  return subs;
+}
+
+void Runtime::run_l2(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep, const Target& t,
+                     std::vector<double>& vals) {
+  DeviceExec& dev = device();
+  const int s = chain.dim - 1;
+  bool explicit_ts = false;
+  if (mode.kind == ExecMode::Kind::Tiled)
+    for (int d = 0; d < chain.dim; ++d) explicit_ts = explicit_ts || mode.tile_sizes[d] > 0;
+  std::vector<L2Sub> subs;
+  std::array<int64_t, kMaxDims> ets{1, 1, 1};
+  if (explicit_ts) {
+    // The reference's tile sizes over the whole chain.
+    for (int d = 0; d < chain.dim; ++d) ets[d] = std::max<int64_t>(1, mode.tile_sizes[d]);
+    for (size_t b = 0; b < chain.size(); b += 32) subs.push_back(L2Sub{b, std::min(chain.size(), b + 32), 0});
+  } else {
+    const uint64_t key = chain.signature() ^ mask_hash(*this, t.masked, t.mask, chain.dim);
+    auto sit = l2_splits_.find(key);
+    if (sit == l2_splits_.end()) sit = l2_splits_.emplace(key, l2_split(chain, t)).first;
+    subs = sit->second;
+  }
+  size_t red_base = 0;
+  for (const L2Sub& sub : subs) {
+    const LoopChain sc = (sub.begin == 0 && sub.end == chain.size()) ? chain : slice(chain, sub.begin, sub.end);
+    std::array<int64_t, kMaxDims> ts = ets;
+    if (!explicit_ts) {
+      for (int d = 0; d < chain.dim; ++d) ts[d] = int64_t{1} << 40;
+      ts[static_cast<size_t>(s)] = sub.ts;
+    }
+    bool hit = false;
+    std::shared_ptr<const TilingPlan> plan = plan_cache_.get_or_build(sc, ts, &hit);
+    if (!hit) {
+      ++rep.plan_constructions;
+      rep.plan_seconds += plan->build_seconds;
+      // execute_plan's pad check (executor.cpp:209-250): every required box
+      // must lie inside the (target's) allocation.
+      std::vector<FieldExtent> fe;
+      for (size_t i = 0; i < t.alloc.size(); ++i) fe.push_back(FieldExtent{fields_[i].name, t.alloc[i]});
+      verify_plan_extents(*plan, fe);
+    }
+    rep.plan_cache_hit = rep.plan_cache_hit && hit;
+    // Items (tile-major, loop order as in execute_plan) with a grid barrier
+    // only where the next item touches what an unsynchronised earlier one
+    // wrote (RAW), reads (WAR) or writes (WAW).
+    auto it = l2_items_.find(plan.get());
+    if (it == l2_items_.end()) {
+      L2Items li;
+      std::vector<DevItem>& items = li.items;
+      std::vector<Footprint> open, all;
+      const int32_t L = plan->num_loops;
+      int32_t flag_off = 0;
+      for (int64_t tt = 0; tt < plan->num_tiles(); ++tt)
+        for (int32_t l = 0; l < L; ++l) {
+          const Range& r = plan->range(tt, l);
+          if (r.empty()) continue;
+          Footprint f = footprint(sc, sc.loops[static_cast<size_t>(l)], r);
+          bool conflict = false;
+          for (const Footprint& o : open)
+            conflict = conflict || overlaps(o.writes, f.reads) || overlaps(o.writes, f.writes) ||
+                       overlaps(o.reads, f.writes);
+          if (conflict && !items.empty()) {
+            items.back().sync = 1;
+            open.clear();
+          }
+          DevItem di{};
+          di.loop = l;
+          di.sync = 0;
+          for (int d = 0; d < 3; ++d) {
+            di.lo[d] = d < chain.dim ? static_cast<int32_t>(r.start(d)) : 0;
+            di.hi[d] = d < chain.dim ? static_cast<int32_t>(r.end(d)) : 1;
+          }
+          // Chunk grid (matches k_l2tiled: 256 points in 1D, 32 x 32 in 2D,
+          // 32 x 8 x 4 in 3D).
+          const int64_t nx = r.extent(0);
+          if (chain.dim == 1) {
+            di.cx = static_cast<int32_t>((nx + 255) / 256);
+            di.cy = 1;
+            di.nch = di.cx;
+          } else if (chain.dim == 2) {
+            di.cx = static_cast<int32_t>((nx + 31) / 32);
+            di.cy = static_cast<int32_t>((r.extent(1) + 31) / 32);
+            di.nch = di.cx * di.cy;
+          } else {
+            di.cx = static_cast<int32_t>((nx + 31) / 32);
+            di.cy = static_cast<int32_t>((r.extent(1) + 7) / 8);
+            di.nch = di.cx * di.cy * static_cast<int32_t>((r.extent(2) + 3) / 4);
+          }
+          di.flag_off = flag_off;
+          flag_off += di.nch;
+          // Dataflow dependencies: every earlier item it conflicts with.
+          di.dep_off = static_cast<int32_t>(li.deps.size());
+          for (size_t j = 0; j < all.size(); ++j)
+            if (overlaps(all[j].writes, f.reads) || overlaps(all[j].writes, f.writes) ||
+                overlaps(all[j].reads, f.writes))
+              li.deps.push_back(static_cast<int32_t>(j));
+          di.ndeps = static_cast<int32_t>(li.deps.size()) - di.dep_off;
+          items.push_back(di);
+          all.push_back(f);
+          open.push_back(std::move(f));
+        }
+      // Stencil reach per dimension (dilation of the dataflow wait).
+      for (const LoopRecord& lp : sc.loops)
+        for (const ArgSpec& a : lp.args) {
+          if (!mode_reads(a.mode)) continue;
+          const Stencil& st = sc.stencil(a.stencil);
+          for (int d = 0; d < chain.dim; ++d)
+            li.reach[static_cast<size_t>(d)] = std::max<int32_t>(
+                li.reach[static_cast<size_t>(d)],
+                static_cast<int32_t>(std::max(std::llabs(st.min_offset(d)), std::llabs(st.max_offset(d)))));
+        }
+      it = l2_items_.emplace(plan.get(), std::move(li)).first;
+    }
+    // Dataflow mode (per-chunk completion flags instead of grid barriers)
+    // is correct but measured slower on the configs (long dependency lists);
+    // opt in with TCG_L2_DATAFLOW=1.
+    static const bool dataflow = [] {
+      const char* e = std::getenv("TCG_L2_DATAFLOW");
+      return e && std::atoi(e) != 0;
+    }();
+    DevChain dc = lower(sc, t);
+    std::vector<double> out(static_cast<size_t>(std::max(1, dc.nred)));
+    static const std::vector<int32_t> no_deps;
+    dev.run_l2(dc, it->second.items, dataflow ? it->second.deps : no_deps, it->second.reach,
+               reinterpret_cast<uint64_t>(plan.get()) ^ (dataflow ? 1 : 0), out.data());
+    for (int i = 0; i < dc.nred; ++i) vals.at(red_base + static_cast<size_t>(i)) = out[static_cast<size_t>(i)];
+    red_base += static_cast<size_t>(dc.nred);
+    last_plan_ = plan;
+    rep.tiles_executed += plan->num_tiles();
+    if (!dataflow)
+      for (const DevItem& di : it->second.items) rep.l2_syncs += di.sync;
+    rep.subchains += 1;
+    rep.ctas += static_cast<int64_t>(it->second.items.size());  // items
+    for (int d = 0; d < chain.dim; ++d) {
+      rep.tile_sizes[d] = std::max(rep.tile_sizes[d], std::min<int64_t>(ts[d], int64_t{1} << 30));
+      rep.max_skew[d] = std::max(rep.max_skew[d], plan->max_skew[d]);
+    }
+  }
+  rep.computed_points += chain_points(chain);
+}
+
 std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode, ExecutionReport& rep,
                                     const Target& t) {
   DeviceExec& dev = device();
@@ -440,67 +724,67 @@ std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode,
   size_t nred = 0;
   for (const LoopRecord& lp : chain.loops) nred += lp.reduction ? 1 : 0;
   std::vector<double> vals(nred, 0.0);
-  // tiled_auto: choose between the windowed-tiled and the untiled executor by
-  // measured device time of this chain signature, then keep the faster.
-  bool use_untiled = mode.kind == ExecMode::Kind::Untiled;
+  // Executor: 0 L2-tiled, 1 untiled, 2 windowed. tiled_auto times every
+  // candidate twice per chain signature (round robin; the first run of each
+  // carries plan construction and lazy module loading) and then keeps the
+  // fastest -- they are all bit-exact.
+  int cand = mode.kind == ExecMode::Kind::Untiled ? 1 : mode.kind == ExecMode::Kind::Windowed ? 2 : 0;
   AutoStat* as = nullptr;
   bool measure = false;
   if (mode.kind == ExecMode::Kind::TiledAuto) {
     as = &auto_[chain.signature() ^ mask_hash(*this, t.masked, t.mask, chain.dim)];
     if (as->ev1) {
+      // Resolve the pending measurement (waits for it: only while tuning).
       float ms = 0;
+      dev.wait_event(as->ev1);
       if (dev.elapsed_ms(as->ev0, as->ev1, &ms)) {
-        if (as->pending_tiled)
-          as->tiled_ms = std::min(as->tiled_ms, ms);
-        else
-          as->untiled_ms = std::min(as->untiled_ms, ms);
+        as->ms[as->pending] = std::min(as->ms[as->pending], ms);
         dev.release(as->ev0);
         dev.release(as->ev1);
         as->ev0 = as->ev1 = nullptr;
       }
     }
+    cand = -1;
     if (!as->ev1) {
-      // Alternate T, U, T, U; each executor's time is the min of its two runs
-      // (the first run of each carries plan construction / lazy module load).
-      const bool t_more = as->tiled_fits && as->tiled_runs < 2;
-      const bool u_more = as->untiled_runs < 2;
-      if (t_more && (as->tiled_runs <= as->untiled_runs || !u_more)) {
-        use_untiled = false;
-        measure = true;
-      } else if (u_more) {
-        use_untiled = true;
-        measure = true;
-      } else {
-        use_untiled = !as->tiled_fits || as->untiled_ms <= as->tiled_ms;
-        if (!as->saved) save_autotune(*as);
-      }
-    } else {
-      use_untiled = !as->tiled_fits || as->untiled_ms <= as->tiled_ms;
+      for (int c = 0; c < kCand; ++c)
+        if (as->fits[c] && as->runs[c] < 2 && (cand < 0 || as->runs[c] < as->runs[cand])) cand = c;
+      measure = cand >= 0;
     }
-    if (measure) {
-      as->ev0 = dev.record();
-      as->pending_tiled = !use_untiled;
-      (use_untiled ? as->untiled_runs : as->tiled_runs)++;
+    if (cand < 0) {
+      cand = as->best();
+      if (!as->ev1 && !as->saved) save_autotune(*as);
     }
   }
+  bool use_untiled = cand == 1;
   if (!use_untiled) {
+    if (measure) as->ev0 = dev.record();
     try {
       rep.tiled = true;
-      rep.executor = "tiled";
-      run_tiled(chain, mode, rep, t, vals);
+      if (cand == 0) {
+        rep.executor = "tiled";
+        run_l2(chain, mode, rep, t, vals);
+      } else {
+        rep.executor = "windowed";
+        run_tiled(chain, mode, rep, t, vals);
+      }
     } catch (const PlanError& e) {
-      // Chains the windowed executor cannot tile at all (e.g. more than 32
-      // datasets) run untiled under tiled_auto; explicit tiled modes raise.
-      if (mode.kind != ExecMode::Kind::TiledAuto || std::string(e.what()).find("does not fit") == std::string::npos)
-        throw;
-      as->tiled_fits = false;
+      // Chains an executor cannot run at all (windows that do not fit,
+      // more than 32 datasets) drop out of tiled_auto; explicit modes raise.
+      if (mode.kind != ExecMode::Kind::TiledAuto) throw;
+      as->fits[cand] = false;
+      if (measure) {
+        dev.release(as->ev0);
+        as->ev0 = nullptr;
+      }
       rep.tiled = false;
       use_untiled = true;
+      cand = 1;
     }
   }
-  if (measure && as && use_untiled && as->pending_tiled) {
-    as->pending_tiled = false;  // fell back: time the untiled run instead
-    as->untiled_runs++;
+  if (measure && as) {
+    if (use_untiled) as->ev0 = as->ev0 ? as->ev0 : dev.record();
+    as->pending = cand;
+    as->runs[cand]++;
   }
   if (use_untiled) {
     rep.executor = "untiled";
@@ -561,8 +845,8 @@ void Runtime::save_autotune(AutoStat& as) {
   if (FILE* f = std::fopen(autotune_file_.c_str(), "w")) {
     for (const auto& [sig, a] : auto_)
       if (a.saved)
-        std::fprintf(f, "%llx %.6f %.6f %d\n", static_cast<unsigned long long>(sig), a.tiled_ms, a.untiled_ms,
-                     a.tiled_fits ? 1 : 0);
+        std::fprintf(f, "%llx %.6f %.6f %.6f %d\n", static_cast<unsigned long long>(sig), a.ms[0], a.ms[1], a.ms[2],
+                     (a.fits[0] ? 1 : 0) | (a.fits[1] ? 2 : 0) | (a.fits[2] ? 4 : 0));
     std::fclose(f);
   }
 }
@@ -938,6 +1222,61 @@ void Runtime::download(DatasetId ds, double* host) {
                      host, f.alloc);
   }
   dev.synchronize();
+}
+
+void Runtime::upload_box(DatasetId ds, const double* host, const Range& box) {
+  flush();
+  const FieldRec& f = fields_.at(static_cast<size_t>(ds));
+  if (!f.alloc.contains(box)) throw AccessError("upload_box: " + box.to_string() + " outside " + f.alloc.to_string());
+  DeviceExec& dev = device();
+  if (!distributed()) {
+    ensure_fields();
+    dev.buf_to_field(f.dev, box, host, box);
+  } else {
+    ensure_dist();
+    for (int r : dist_->local) {
+      const Target& t = dist_->targets[static_cast<size_t>(r)];
+      const Range part = t.alloc[static_cast<size_t>(ds)].intersect(box);
+      if (!part.empty()) dev.buf_to_field(t.dev[static_cast<size_t>(ds)], part, host, box);
+    }
+  }
+  dev.synchronize();
+}
+
+void Runtime::download_box(DatasetId ds, double* host, const Range& box) {
+  flush();
+  const FieldRec& f = fields_.at(static_cast<size_t>(ds));
+  if (!f.alloc.contains(box)) throw AccessError("download_box: " + box.to_string() + " outside " + f.alloc.to_string());
+  DeviceExec& dev = device();
+  if (!distributed()) {
+    ensure_fields();
+    dev.field_to_buf(f.dev, box, host, box);
+  } else {
+    ensure_dist();
+    for (int pass = 0; pass < 2; ++pass)
+      for (int r : dist_->local) {
+        const Target& t = dist_->targets[static_cast<size_t>(r)];
+        const Range part = (pass == 0 ? t.alloc[static_cast<size_t>(ds)]
+                                      : dist_->layout.owned[static_cast<size_t>(r)].intersect(f.logical))
+                               .intersect(box);
+        if (!part.empty()) dev.field_to_buf(t.dev[static_cast<size_t>(ds)], part, host, box);
+      }
+  }
+  dev.synchronize();
+}
+
+Range Runtime::local_box(DatasetId ds) {
+  const FieldRec& f = fields_.at(static_cast<size_t>(ds));
+  if (!distributed()) return f.alloc;
+  const RankLayout& lay = rank_layout();
+  std::vector<int> local;
+  if (proc_rank_ >= 0)
+    local = {proc_rank_};
+  else
+    for (int r = 0; r < lay.rank_count(); ++r) local.push_back(r);
+  Range h = rank_alloc(lay, local[0], f.pad).intersect(f.alloc);
+  for (int r : local) h = h.hull(rank_alloc(lay, r, f.pad).intersect(f.alloc));
+  return h;
 }
 
 void Runtime::fill_logical(DatasetId ds, double v) {

@@ -30,12 +30,18 @@ struct RuntimeConfig {
 };
 
 struct ExecMode {
-  enum class Kind : uint8_t { Untiled = 0, Tiled = 1, TiledAuto = 2 };
+  // Untiled / Tiled / TiledAuto are the reference's modes (runtime.hpp:25-35).
+  // Tiled runs the reference tile plan with the L2-resident executor
+  // (tile_sizes as in the reference; 0 = GPU sizer). Windowed is the
+  // shared-memory windowed executor (tile_sizes = column block / stream tile
+  // upper bounds; 0 = sizer).
+  enum class Kind : uint8_t { Untiled = 0, Tiled = 1, TiledAuto = 2, Windowed = 3 };
   Kind kind = Kind::Untiled;
   std::array<int64_t, kMaxDims> tile_sizes{0, 0, 0};
   static ExecMode untiled() { return {}; }
   static ExecMode tiled(const std::array<int64_t, kMaxDims>& ts) { return {Kind::Tiled, ts}; }
   static ExecMode tiled_auto() { return {Kind::TiledAuto, {0, 0, 0}}; }
+  static ExecMode windowed(const std::array<int64_t, kMaxDims>& ts) { return {Kind::Windowed, ts}; }
 };
 
 struct LoopExecStats {
@@ -64,6 +70,7 @@ struct ExecutionReport {
   int64_t ctas = 0;
   int64_t subchains = 0;
   int64_t computed_points = 0;
+  int64_t l2_syncs = 0;  // grid barriers of the L2-tiled executor
   std::string executor = "untiled";  // executor that ran the chain (tiled_auto may pick either)
   std::array<int, kMaxDims> cta_grid{1, 1, 1};
   int64_t total_points() const;
@@ -96,6 +103,13 @@ class Runtime {
   // the reference Field layout, field.cpp:22-26). Flush first.
   void upload(DatasetId ds, const double* host);
   void download(DatasetId ds, double* host);
+  // Box forms: `host` is dense over `box` (inside the allocation). In a
+  // distributed runtime only the parts held by this process's ranks move.
+  void upload_box(DatasetId ds, const double* host, const Range& box);
+  void download_box(DatasetId ds, double* host, const Range& box);
+  // The part of ds's allocation this process holds: the whole allocation,
+  // or the hull of its ranks' allocations (clipped to the field's).
+  Range local_box(DatasetId ds);
 
   // Distribution over a rank grid (reference Runtime::set_rank_grid,
   // runtime.hpp:77-81, runtime.cpp:213-222). set_rank_grid hosts every rank
@@ -169,6 +183,13 @@ class Runtime {
   DevChain lower(const LoopChain& chain, const Target& t) const;
   void run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep, const Target& t,
                  std::vector<double>& vals);
+  void run_l2(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep, const Target& t,
+              std::vector<double>& vals);
+  struct L2Sub {
+    size_t begin, end;  // loops [begin, end)
+    int64_t ts;         // slowest-dim tile size
+  };
+  std::vector<L2Sub> l2_split(const LoopChain& chain, const Target& t) const;
   void store(const std::vector<ReductionHandle>& handles, const double* vals);
 
   int dim_;
@@ -183,17 +204,29 @@ class Runtime {
   std::map<std::tuple<uint64_t, int64_t, int64_t, int64_t, int>, std::shared_ptr<const GpuTiledPlan>> gpu_plans_;
   int64_t gpu_plan_builds_ = 0;
   std::shared_ptr<const GpuTiledPlan> last_gpu_plan_;
+  std::shared_ptr<const TilingPlan> last_plan_;
+  struct L2Items {
+    std::vector<DevItem> items;
+    std::vector<int32_t> deps;
+    std::array<int32_t, 3> reach{0, 0, 0};
+  };
+  std::map<const TilingPlan*, L2Items> l2_items_;
+  std::map<uint64_t, std::vector<L2Sub>> l2_splits_;
   ExecutionReport last_report_;
   // tiled_auto: per chain signature, device time of the windowed-tiled and the
   // untiled executor (both bit-exact); later flushes use the faster one.
+  // tiled_auto: per chain signature, device time of each executor candidate
+  // (0 L2-tiled, 1 untiled, 2 windowed); all bit-exact, the fastest is kept.
+  static constexpr int kCand = 3;
   struct AutoStat {
-    int tiled_runs = 0, untiled_runs = 0;
-    float tiled_ms = 1e30f, untiled_ms = 1e30f;
-    bool tiled_fits = true;
+    int runs[kCand] = {0, 0, 0};
+    float ms[kCand] = {1e30f, 1e30f, 1e30f};
+    bool fits[kCand] = {true, true, true};
     void* ev0 = nullptr;
     void* ev1 = nullptr;
-    bool pending_tiled = false;
+    int pending = -1;    // candidate being timed
     bool saved = false;  // decision final (and written to TCG_AUTOTUNE_FILE)
+    int best() const;
   };
   void save_autotune(AutoStat& as);
   std::map<uint64_t, AutoStat> auto_;

@@ -36,6 +36,7 @@ tcg::ExecMode mode_of(int mode, const int64_t* ts) {
   if (mode == TCG_UNTILED) return tcg::ExecMode::untiled();
   if (mode == TCG_TILED) return tcg::ExecMode::tiled({ts[0], ts[1], ts[2]});
   if (mode == TCG_TILED_AUTO) return tcg::ExecMode::tiled_auto();
+  if (mode == TCG_WINDOWED) return tcg::ExecMode::windowed({ts[0], ts[1], ts[2]});
   throw tcg::InvalidArgument("unknown exec mode " + std::to_string(mode));
 }
 
@@ -247,7 +248,7 @@ int tcg_gpu_plan_pending(tcg_runtime* rt, int mode, const int64_t ts[3], char* b
     tcg::LoopChain c = rt->rt->take_pending();
     const int s = c.dim - 1;
     tcg::GpuTileChoice choice;
-    if (mode == TCG_TILED)
+    if (mode == TCG_WINDOWED)
       for (int d = 0; d < c.dim; ++d) {
         if (d == s)
           choice.stream_tile = std::max<int64_t>(1, ts[d]);
@@ -300,6 +301,24 @@ int tcg_gpu_plan_pending(tcg_runtime* rt, int mode, const int64_t ts[3], char* b
 
 int tcg_set_rank_grid(tcg_runtime* rt, const int32_t grid[3]) {
   return guard([&] { rt->rt->set_rank_grid({grid[0], grid[1], grid[2]}); });
+}
+
+int tcg_upload_box(tcg_runtime* rt, int32_t ds, const double* host, const int64_t box[6]) {
+  return guard([&] { rt->rt->upload_box(ds, host, range6(rt->rt->dim(), box)); });
+}
+
+int tcg_download_box(tcg_runtime* rt, int32_t ds, double* host, const int64_t box[6]) {
+  return guard([&] { rt->rt->download_box(ds, host, range6(rt->rt->dim(), box)); });
+}
+
+int tcg_local_box(tcg_runtime* rt, int32_t ds, int64_t out[6]) {
+  return guard([&] {
+    const tcg::Range b = rt->rt->local_box(ds);
+    for (int d = 0; d < 3; ++d) {
+      out[2 * d] = d < b.dim() ? b.start(d) : 0;
+      out[2 * d + 1] = d < b.dim() ? b.end(d) : 1;
+    }
+  });
 }
 
 int tcg_rank_owned(tcg_runtime* rt, int32_t rank, int64_t out[6]) {

@@ -103,6 +103,9 @@ def load_library() -> ctypes.CDLL:
                                                 ctypes.POINTER(_I64)]),
         "tcg_signature_pending": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
         "tcg_set_rank_grid": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
+        "tcg_upload_box": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_I64)]),
+        "tcg_download_box": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_I64)]),
+        "tcg_local_box": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_I64)]),
         "tcg_rank_owned": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_I64)]),
         "tcg_comm_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
         "tcg_set_process_rank": (ctypes.c_int, [_P, ctypes.POINTER(_I32), _I32, ctypes.c_char_p]),
@@ -243,6 +246,13 @@ class ExecMode:
     def tiled_auto():
         return ExecMode(2, (0, 0, 0))
 
+    @staticmethod
+    def windowed(ts=(0, 0, 0)):
+        """The shared-memory windowed executor (B200-specific; ts = column
+        block / stream tile upper bounds, 0 = sizer)."""
+        ts = list(ts) + [0] * (3 - len(ts))
+        return ExecMode(3, tuple(int(v) for v in ts[:3]))
+
 
 @dataclass
 class RuntimeConfig:
@@ -305,6 +315,9 @@ class Runtime:
         self.config = cfg
         self._allocs: list[Range] = []
         self._logicals: list[Range] = []
+        self._enc: dict = {}
+        self._out = _I32(-1)
+        self._out_ref = ctypes.byref(self._out)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -350,17 +363,20 @@ class Runtime:
     def par_loop(self, kernel: KernelHandle, rng: Range, args: Sequence, reduction: Optional[int] = None) -> int:
         if rng.dim != self.dim:
             raise InvalidArgument("par_loop: range dim does not match block")
-        flat = []
-        for a in args:
-            if isinstance(a, ArgSpec):
-                flat += [a.dataset, a.stencil, int(a.mode)]
-            else:
-                flat += [int(a[0]), int(a[1]), int(a[2])]
-        prm = list(kernel.params)
-        out = _I32(-1)
-        _check(self._lib.tcg_par_loop(self._h, kernel.id, kernel.body, _arr(_I64, rng.lohi), len(args),
-                                      _arr(_I32, flat), -1 if reduction is None else int(reduction), len(prm),
-                                      _arr(_D, prm), ctypes.byref(out)))
+        # Encoded ctypes arguments are cached per (range, args, params): a
+        # time-stepping code re-enqueues the same loops every step.
+        key = (tuple(rng.lohi), tuple((a.dataset, a.stencil, int(a.mode)) if isinstance(a, ArgSpec)
+                                      else (int(a[0]), int(a[1]), int(a[2])) for a in args), tuple(kernel.params))
+        enc = self._enc.get(key)
+        if enc is None:
+            flat = [v for t in key[1] for v in t]
+            enc = (_arr(_I64, key[0]), len(key[1]), _arr(_I32, flat), len(key[2]), _arr(_D, key[2]))
+            if len(self._enc) > 4096:
+                self._enc.clear()
+            self._enc[key] = enc
+        out = self._out
+        _check(self._lib.tcg_par_loop(self._h, kernel.id, kernel.body, enc[0], enc[1], enc[2],
+                                      -1 if reduction is None else int(reduction), enc[3], enc[4], self._out_ref))
         return out.value
 
     def flush(self, mode: Optional[ExecMode] = None) -> dict:
@@ -409,6 +425,26 @@ class Runtime:
         out = np.empty(a.shape(), dtype=np.float64)
         _check(self._lib.tcg_download(self._h, ds, out.ctypes.data_as(_P)))
         return out
+
+    def upload_box(self, ds: int, data: np.ndarray, box: Range) -> None:
+        arr = np.ascontiguousarray(data, dtype=np.float64)
+        if arr.size != box.volume():
+            raise InvalidArgument(f"upload_box: expected {box.volume()} values for {box}, got {arr.size}")
+        _check(self._lib.tcg_upload_box(self._h, ds, arr.ctypes.data_as(_P), _arr(_I64, box.lohi)))
+
+    def download_box(self, ds: int, box: Range, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(box.shape(), dtype=np.float64)
+        if not out.flags.c_contiguous or out.size != box.volume() or out.dtype != np.float64:
+            raise InvalidArgument("download_box: out must be a C-contiguous float64 array over the box")
+        _check(self._lib.tcg_download_box(self._h, ds, out.ctypes.data_as(_P), _arr(_I64, box.lohi)))
+        return out
+
+    def local_box(self, ds: int) -> Range:
+        """The part of ds's allocation this process holds."""
+        a = (_I64 * 6)()
+        _check(self._lib.tcg_local_box(self._h, ds, a))
+        return Range(self.dim, list(a))
 
     def synchronize(self) -> None:
         _check(self._lib.tcg_synchronize(self._h))

@@ -14,7 +14,7 @@ from paper_1704_00693_b200 import ExecMode, Range, Runtime, comm_unique_id, conf
 
 pytestmark = pytest.mark.gpu
 
-MODES = [ExecMode.untiled(), ExecMode.tiled((0, 0, 0)), ExecMode.tiled_auto()]
+MODES = [ExecMode.untiled(), ExecMode.tiled((0, 0, 0)), ExecMode.windowed(), ExecMode.tiled_auto()]
 
 
 class _GridRuntime(Runtime):
@@ -23,7 +23,7 @@ class _GridRuntime(Runtime):
         self.set_rank_grid(grid)
 
 
-@pytest.mark.parametrize("mode", MODES, ids=["untiled", "tiled", "auto"])
+@pytest.mark.parametrize("mode", MODES, ids=["untiled", "tiled", "windowed", "auto"])
 @pytest.mark.parametrize("seed,dim,grid", [(31, 2, (1, 2, 1)), (32, 2, (1, 4, 1)), (33, 2, (2, 2, 1)),
                                            (34, 3, (1, 1, 2)), (35, 3, (1, 2, 2)), (36, 1, (3, 1, 1))])
 def test_random_chains_on_rank_grid_match_oracle(oracle_lib, mode, seed, dim, grid):
@@ -33,7 +33,7 @@ def test_random_chains_on_rank_grid_match_oracle(oracle_lib, mode, seed, dim, gr
     C.assert_same(got, want, f"seed {seed} grid {grid}")
 
 
-@pytest.mark.parametrize("mode", MODES, ids=["untiled", "tiled", "auto"])
+@pytest.mark.parametrize("mode", MODES, ids=["untiled", "tiled", "windowed", "auto"])
 def test_repeated_chains_use_write_history(oracle_lib, mode):
     # Second and third flushes see the first's writes in the history
     # (exchange_flags, dist.cpp:79-115): still exact.

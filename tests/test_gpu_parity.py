@@ -15,7 +15,10 @@ pytestmark = pytest.mark.gpu
 
 MODES = {
     "untiled": lambda dim, seed: ExecMode.untiled(),
+    # the reference's tile plans with random tile sizes, L2-resident executor
     "tiled": lambda dim, seed: ExecMode.tiled(C.random_tile_sizes(seed, dim)),
+    "tiled_sizer": lambda dim, seed: ExecMode.tiled((0, 0, 0)),
+    "windowed": lambda dim, seed: ExecMode.windowed(C.random_tile_sizes(seed, dim)),
     "auto": lambda dim, seed: ExecMode.tiled_auto(),
 }
 
@@ -42,13 +45,13 @@ def test_random_chains_stream_segments(oracle_lib, segments):
         gc = C.generate(seed, dim=2)
         want = C.run(oracle_lib.OracleRuntime(2), gc, None)
         got = C.run(Runtime(2, RuntimeConfig(stream_segments=segments)), gc,
-                    ExecMode.tiled(C.random_tile_sizes(seed, 2)))
+                    ExecMode.windowed(C.random_tile_sizes(seed, 2)))
         C.assert_same(got, want, f"segments{segments} seed{seed}")
 
 
 @pytest.mark.parametrize("copy", [True, False])
 @pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((16, 16, 1)), ExecMode.tiled((8, 4, 1)),
-                                  ExecMode.tiled_auto()])
+                                  ExecMode.windowed((16, 16, 1)), ExecMode.tiled_auto()])
 def test_jacobi_app_matches_reference_app(ref_lib, copy, mode):
     want = ref_lib.ref_app_jacobi(64, 64, 10, copy)
     rt = Runtime(2)
@@ -60,7 +63,7 @@ def test_jacobi_app_matches_reference_app(ref_lib, copy, mode):
 
 
 @pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((8, 8, 1)), ExecMode.tiled((48, 16, 1)),
-                                  ExecMode.tiled_auto()])
+                                  ExecMode.windowed((48, 16, 1)), ExecMode.tiled_auto()])
 def test_minihydro_app_matches_reference_app(ref_lib, mode):
     fields, monitors = ref_lib.ref_app_minihydro(48, 48, 3)
     rt = Runtime(2)
@@ -92,7 +95,8 @@ def _run_config(rt, cfg_cls, n, **kw):
 
 
 @pytest.mark.parametrize("cfg,n", [(configs.HeatC1, 64), (configs.HydroC2, 96), (configs.Jacobi3DC3, 24)])
-@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled_auto()])
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((0, 0, 0)), ExecMode.windowed(),
+                                  ExecMode.tiled_auto()])
 def test_configs_small_match_oracle(oracle_lib, cfg, n, mode):
     want = _run_config(oracle_lib.OracleRuntime(3 if cfg is configs.Jacobi3DC3 else 2), cfg, n)
     got = _run_config(Runtime(3 if cfg is configs.Jacobi3DC3 else 2), cfg, n, mode=mode)
@@ -101,7 +105,7 @@ def test_configs_small_match_oracle(oracle_lib, cfg, n, mode):
     assert got[1] == want[1]
 
 
-@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled_auto()])
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((0, 0, 0)), ExecMode.tiled_auto()])
 def test_cg_residual_history_matches_reference(ref_lib, mode):
     # c4 at 64^2: the residual history must agree to 1e-10 relative over the
     # window where the reference is self-consistent (SURVEY.md §7 hard parts).
@@ -146,9 +150,9 @@ def test_fetch_reduction_flushes_prefix_only():
 
 
 def test_tiled_auto_switches_executor_bit_exact(oracle_lib):
-    # tiled_auto times both executors per chain signature (tiled, untiled,
-    # tiled, untiled) and keeps the faster; every flush must stay bit-exact.
-    steps = 8
+    # tiled_auto times the executors per chain signature (L2-tiled, untiled,
+    # windowed, twice each) and keeps the fastest; every flush bit-exact.
+    steps = 10
     want = _run_config(oracle_lib.OracleRuntime(2), configs.HydroC2, 96, steps=steps)
     rt = Runtime(2)
     rt.set_default_mode(ExecMode.tiled_auto())
@@ -157,16 +161,16 @@ def test_tiled_auto_switches_executor_bit_exact(oracle_lib):
     for _ in range(steps):
         mins.append(rt.fetch_reduction(c.enqueue_step()))
         used.append(parse_report(rt.report_text())["executor"])
-    assert used[:4] == ["tiled", "untiled", "tiled", "untiled"], used
-    assert len(set(used[4:])) == 1, used
+    assert used[:6] == ["tiled", "untiled", "windowed"] * 2, used
+    assert len(set(used[6:])) == 1, used
     got = c.outputs()
     for k in want[0]:
         assert np.array_equal(got[k], want[0][k]), k
     assert mins == want[1]
 
 
-@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((0, 0, 0)), ExecMode.tiled_auto()],
-                         ids=["untiled", "tiled", "auto"])
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((0, 0, 0)), ExecMode.windowed(),
+                                  ExecMode.tiled_auto()], ids=["untiled", "tiled", "windowed", "auto"])
 def test_empty_range_loops(oracle_lib, mode):
     # A loop with an empty range does nothing; a reducing one yields the
     # identity (reduce_identity, types.hpp:272-288).

@@ -10,4 +10,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_untiled -s 60 -c 14 -o gpurun_out/c2_untiled -f \
   python bench.py --steps 5 --warmup 3 --mode untiled --no-cpu-baseline --no-e2e --no-untiled > gpurun_out/ncu_full_u.log 2>&1; echo "ncu2 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tiled -s 4 -c 2 -o gpurun_out/c2_tiled -f \
-  python bench.py --steps 5 --warmup 3 --mode tiled:0,0,0 --no-cpu-baseline --no-e2e --no-untiled > gpurun_out/ncu_full_t.log 2>&1; echo "ncu3 rc=$?"
+  python bench.py --steps 5 --warmup 3 --mode windowed --no-cpu-baseline --no-e2e --no-untiled > gpurun_out/ncu_full_t.log 2>&1; echo "ncu3 rc=$?"
