@@ -126,6 +126,8 @@ def make_config(name, rt, n=None, ny=None):
         return configs.Jacobi3DC3(rt, n or 512)
     if name == "c4":
         return configs.CgC4(rt, n or 4096)
+    if name == "c5":
+        return configs.NsC5(rt, n or 768)
     raise ValueError(name)
 
 
@@ -139,7 +141,7 @@ class Step:
 
     def __call__(self):
         c, rt = self.cfg, self.rt
-        if self.name == "c2":
+        if self.name in ("c2", "c5"):
             rt.fetch_reduction(c.enqueue_step())
         elif self.name in ("c1", "c3"):
             c.enqueue_chain()
@@ -150,12 +152,13 @@ class Step:
     def cell_updates(self):
         c = self.cfg
         return {"c2": lambda: c.cell_updates_per_step(), "c1": lambda: c.cell_updates_per_chain(),
-                "c3": lambda: c.cell_updates_per_chain(), "c4": lambda: c.cell_updates_per_iteration()}[self.name]()
+                "c3": lambda: c.cell_updates_per_chain(), "c4": lambda: c.cell_updates_per_iteration(),
+                "c5": lambda: c.cell_updates_per_step()}[self.name]()
 
     def algorithmic_bytes(self):
         c = self.cfg
         return {"c2": lambda: c.bytes_per_step(), "c1": lambda: c.bytes_per_chain(), "c3": lambda: c.bytes_per_chain(),
-                "c4": lambda: c.bytes_per_iteration()}[self.name]()
+                "c4": lambda: c.bytes_per_iteration(), "c5": lambda: c.bytes_per_step()}[self.name]()
 
     def compulsory_bytes(self):
         """Bytes a perfectly fused chain must move: each seeded dataset read
@@ -167,6 +170,9 @@ class Step:
             return 3 * 8 * c.n * c.n
         if self.name == "c3":
             return 3 * 8 * c.inner.volume()
+        if self.name == "c5":
+            # per RK stage every one of the 15 fields read once, 10 written once
+            return 3 * (15 + 10) * 8 * c.n ** 3
         return 4 * 8 * c.n * c.n * 4 // 2
 
 
@@ -176,6 +182,8 @@ WORKLOAD_TEXT = {
     "c1": "c1_heat2d: fp64 1024^2, u U[0,1) seed 42, 20-loop chains (10 timesteps of lap + copy)",
     "c3": "c3_jacobi3d: fp64 512^3, 16-loop chains (8 sweeps a->b->a)",
     "c4": "c4_cg2d: fp64 4096^2 CG, 4 loops + 2 dot reductions per iteration",
+    "c5": "c5_ns3d: fp64 768^3 periodic Taylor-Green vortex, 15 fields, 4th-order star2 differences, RK3: "
+          "22 loops + 3 periodic ghost fills + kinetic-energy sum per step",
 }
 
 
@@ -259,9 +267,10 @@ def cpu_reference(cfg_name, k, warmup, budget_s=120.0, mode_pick=None, ny=None):
     if mode_pick:
         modes = [m for m in modes if m[0] == mode_pick]
     for mname, mode in modes:
-        rt = pyoracle.RefRuntime(2 if cfg_name != "c3" else 3, threads=threads)
+        rt = pyoracle.RefRuntime(3 if cfg_name in ("c3", "c5") else 2, threads=threads)
         rt.set_default_mode(mode)
-        cfg = make_config(cfg_name, rt, ny=ny)
+        # c5 at 768^3 needs ~62 GB of host fields: the CPU sample runs 128^3.
+        cfg = make_config(cfg_name, rt, n=128 if cfg_name == "c5" else None, ny=ny)
         st = Step(cfg_name, cfg, rt)
         t0 = time.perf_counter()
         st()  # probe step (also warm-up)
@@ -277,7 +286,9 @@ def cpu_reference(cfg_name, k, warmup, budget_s=120.0, mode_pick=None, ny=None):
         del rt
     v, mname, n, dt = best
     return {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{n} full {cfg_name} steps at BASELINE size ({dt:.1f} s), reference tilechain "
+            "sample": f"{n} full {cfg_name} steps at "
+                      f"{'128^3 (BASELINE 768^3 does not fit host RAM)' if cfg_name == 'c5' else 'BASELINE size'} "
+                      f"({dt:.1f} s), reference tilechain "
                       f"RuntimeConfig.threads={threads}, best of untiled/tiled_auto = {mname}"}, None
 
 
@@ -305,7 +316,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--mode", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -320,6 +331,8 @@ def main():
     # of the same command (kernels serialised, timings distorted) executes
     # the choices the timed run made.
     os.environ.setdefault("TCG_AUTOTUNE_FILE", str(REPO / f".tcg_autotune_{args.config}"))
+    if os.environ.get("NCCL_DEBUG", "VERSION") == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
     world, rank, local, dist = dist_setup(args.gpus)
     if args.impl == "reference":
         return run_reference_arm(args, world, rank, dist)
@@ -345,7 +358,7 @@ def main():
         return obj[0]
 
     def build(m):
-        rt = Runtime(3 if args.config == "c3" else 2)
+        rt = Runtime(3 if args.config in ("c3", "c5") else 2)
         if sharded:
             rt.set_process_rank((1, world, 1), rank, new_comm_id())
         rt.set_default_mode(m)
@@ -357,20 +370,23 @@ def main():
     for _ in range(args.warmup):
         step()
     barrier(dist)
-    rt.set_timing(True)
     l0 = rt.launches()
     with ClockSampler(local) as clk:
         ms = time_steps(rt, step, args.steps)
     launches = rt.launches() - l0
-    kt = rt.kernel_timing()
-    rt.set_timing(False)
     ms = max_over_ranks(ms, dist)
     # Whole-job cell-updates per step: the sharded domain counts once; each
     # replica counts its own.
     cu = step.cell_updates() if sharded else step.cell_updates() * world
     value = cu * args.steps / (ms / 1e3)
     report = pkg.parse_report(rt.report_text())
-
+    # Kernel durations for the roofline: the same K steps again with CUDA
+    # events around every executor kernel on the executor stream (kept out of
+    # the `value` run: the per-kernel event records cost host time per launch).
+    rt.set_timing(True)
+    ms_instr = time_steps(rt, step, args.steps)
+    kt = rt.kernel_timing()
+    rt.set_timing(False)
     # The dominant kernel: tiled_auto may settle on either executor per chain.
     tiled = kt["tiled_ms"] > kt["untiled_ms"]
     kname = "k_tiled" if tiled else "k_untiled"
@@ -387,7 +403,10 @@ def main():
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic,
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": per_launch_alg,
-                "avg_launch_ms": avg_ms, "launches": kn, "kernel_share_of_step": kms / ms if ms else None,
+                "avg_launch_ms": avg_ms, "launches": kn,
+                "kernel_share_of_step": kms / ms_instr if ms_instr else None,
+                "timing": "per-kernel CUDA events on the executor stream over a repeat of the K timed steps "
+                          f"({ms_instr / args.steps:.4f} ms/step instrumented)",
                 "compulsory_bytes_per_launch": comp * args.steps / max(kn, 1),
                 "frac_compulsory": (comp * args.steps / max(kn, 1)) / (avg_ms / 1e3) / 1e9 / peak if kn else None,
                 "note": "achieved = untiled-chain (algorithmic) bytes / kernel time; >1 means on-chip reuse. "
@@ -412,7 +431,10 @@ def main():
 
     # ---- end-to-end through the public API with host buffers --------------------
     e2e = None
-    if not args.no_e2e:
+    if args.config == "c5" and not args.no_e2e:
+        e2e = {"value": None, "note": "c5's five 4.2 GB conserved fields are generated slab by slab on the host; "
+                                      "an end-to-end leg would need ~21 GB of pinned host copies -- skipped"}
+    elif not args.no_e2e:
         rte, cfge, stepe = build(mode)
         ids = list(cfge.init.keys())
         boxes = getattr(cfge, "init_box", {})

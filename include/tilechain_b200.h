@@ -106,6 +106,10 @@ int tcg_pending_loops(tcg_runtime* rt, int64_t* out);
 int tcg_get(tcg_runtime* rt, int32_t ds, const int64_t p[3], double* out);
 int tcg_put(tcg_runtime* rt, int32_t ds, const int64_t p[3], double v);
 int tcg_fill_logical(tcg_runtime* rt, int32_t ds, double v);
+/* Periodic ghost copy (depth <= pad) of n fields, all dimensions; flushes
+ * first. No reference counterpart (the reference has no periodic support);
+ * c5 needs it. */
+int tcg_periodic_fill(tcg_runtime* rt, int n, const int32_t* ds, int64_t depth);
 /* host: dense fp64 over the allocation range, dim 0 fastest. */
 int tcg_upload(tcg_runtime* rt, int32_t ds, const double* host);
 int tcg_download(tcg_runtime* rt, int32_t ds, double* host);

@@ -162,6 +162,32 @@ class _Base:
     def alloc_range(self, ds):
         return self._allocs[ds]
 
+    def periodic_fill(self, datasets, depth, logical):
+        """Host ghost copy for a periodic box (the SURVEY §8(c) recipe for c5:
+        pure copying into the padding, so bit-exact), dimension by dimension
+        like Runtime::periodic_fill. `logical`: lohi list of the box."""
+        self.flush()
+        L = [logical[2 * d] for d in range(self.dim)]
+        H = [logical[2 * d + 1] for d in range(self.dim)]
+        for ds in datasets:
+            al = self._allocs[ds]
+            arr = self.download(ds)
+            lo = [al.start(d) for d in range(self.dim)]
+            for d in range(self.dim):
+                def sl(a, b, dd=d):
+                    idx = []
+                    for e in reversed(range(self.dim)):
+                        if e == dd:
+                            idx.append(slice(a - lo[e], b - lo[e]))
+                        elif e < dd:
+                            idx.append(slice(L[e] - depth - lo[e], H[e] + depth - lo[e]))
+                        else:
+                            idx.append(slice(L[e] - lo[e], H[e] - lo[e]))
+                    return tuple(idx)
+                arr[sl(L[d] - depth, L[d])] = arr[sl(H[d] - depth, H[d])]
+                arr[sl(H[d], H[d] + depth)] = arr[sl(L[d], L[d] + depth)]
+            self.upload(ds, arr)
+
 
 class RefRuntime(_Base):
     """The reference tilechain::Runtime (threads = CPU workers)."""

@@ -394,3 +394,117 @@ class CgC4:
 
 
 CONFIGS = {c.name: c for c in (HeatC1, HydroC2, Jacobi3DC3, CgC4)}
+
+
+# ---------------------------------------------------------------------------
+# BASELINE config c5: 3D compressible Navier-Stokes-like Taylor-Green vortex.
+
+class NsC5:
+    """Periodic 2*pi box, n^3 points x_i = i*h; rho = 1, u = sin x cos y cos z,
+    v = -cos x sin y cos z, w = 0, p = 100/1.4 + (cos 2x + cos 2y)(cos 2z + 2)/16;
+    4th-order central differences (radius-2 star per axis), Re = 1600,
+    Pr = 0.71, low-storage RK3 (Williamson). Per step 3 stages x [prim,
+    periodic ghost fill, 5 RHS loops, update] + a kinetic-energy Sum = 22
+    loops (csrc/kernels/tc_ns.h). Initial values are computed on the host
+    (numpy sin/cos) and uploaded identically to every executor and the
+    oracle; the bench uploads them slab by slab."""
+
+    name = "c5_ns3d"
+    GAMMA = 1.4
+    RK_A = (0.0, -5.0 / 9.0, -153.0 / 128.0)
+    RK_B = (1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0)
+
+    def __init__(self, rt, n=768, re=1600.0, pr=0.71, cfl=0.3, slab=16):
+        self.rt, self.n = rt, n
+        g = self.GAMMA
+        self.h = 2.0 * math.pi / n
+        self.inv12h = 1.0 / (12.0 * self.h)
+        self.inv12h2 = 1.0 / (12.0 * self.h * self.h)
+        self.mu = 1.0 / re
+        self.kappa = self.mu * g / ((g - 1.0) * pr)
+        self.p0 = 100.0 / g
+        self.dt = cfl * self.h / (1.0 + math.sqrt(g * self.p0))
+        pts = [(0, 0, 0)]
+        for d in range(3):
+            for k in (-2, -1, 1, 2):
+                p = [0, 0, 0]
+                p[d] = k
+                pts.append(tuple(p))
+        self.star = rt.declare_stencil("star2_3d", pts)
+        self.pt = rt.declare_stencil("point", [(0, 0, 0)])
+        self.dom = Range.d3(0, n, 0, n, 0, n)
+        names = ["rho", "mx", "my", "mz", "E", "d_rho", "d_mx", "d_my", "d_mz", "d_E", "u", "v", "w", "p", "T"]
+        self.f = {nm: rt.declare_field(nm, self.dom) for nm in names}
+        al = rt.alloc_range(self.f["rho"])
+        box = rt.local_box(self.f["rho"]) if hasattr(rt, "local_box") else al
+        # Host initial condition, slab by slab along z (a full 768^3 field is
+        # 4.2 GB; the bench never holds all five at once).
+        whole = box == al and al.volume() * 8 * 5 < (1 << 31)
+        z0, z1 = box.start(2), box.end(2)
+        for zs in range(z0, z1, (z1 - z0) if whole else slab):
+            ze = min(z1, zs + ((z1 - z0) if whole else slab))
+            sb = Range.d3(box.start(0), box.end(0), box.start(1), box.end(1), zs, ze)
+            vals = self._initial(sb)
+            for nm, arr in vals.items():
+                if whole:
+                    rt.upload(self.f[nm], arr)
+                else:
+                    rt.upload_box(self.f[nm], arr, sb)
+        self.logical = list(self.dom.lohi)
+
+    def _initial(self, sb):
+        """Conserved fields over box sb (zero outside the logical box)."""
+        n, h, g = self.n, self.h, self.GAMMA
+        zi = np.arange(sb.start(2), sb.end(2))
+        yi = np.arange(sb.start(1), sb.end(1))
+        xi = np.arange(sb.start(0), sb.end(0))
+        Z, Y, X = np.meshgrid(zi, yi, xi, indexing="ij")
+        inside = (X >= 0) & (X < n) & (Y >= 0) & (Y < n) & (Z >= 0) & (Z < n)
+        x, y, z = X * h, Y * h, Z * h
+        u = np.sin(x) * np.cos(y) * np.cos(z)
+        v = -np.cos(x) * np.sin(y) * np.cos(z)
+        w = np.zeros_like(u)
+        rho = np.ones_like(u)
+        p = self.p0 + (np.cos(2.0 * x) + np.cos(2.0 * y)) * (np.cos(2.0 * z) + 2.0) / 16.0
+        E = p / (g - 1.0) + 0.5 * rho * ((u * u + v * v) + w * w)
+        out = {"rho": rho, "mx": rho * u, "my": rho * v, "mz": rho * w, "E": E}
+        for k in out:
+            out[k] = np.where(inside, out[k], 0.0)
+        return out
+
+    def enqueue_step(self) -> int:
+        rt, f, S, P, dom = self.rt, self.f, self.star, self.pt, self.dom
+        U = [f["rho"], f["mx"], f["my"], f["mz"], f["E"]]
+        dU = [f["d_rho"], f["d_mx"], f["d_my"], f["d_mz"], f["d_E"]]
+        vel = [f["u"], f["v"], f["w"]]
+        for s in range(3):
+            a, b = self.RK_A[s], self.RK_B[s]
+            rt.par_loop(KernelHandle(K.NS_PRIM, "ns_prim", K.NS_PRIM, (self.GAMMA - 1.0,)), dom,
+                        [ArgSpec(x, P, R) for x in U] + [ArgSpec(f[nm], P, W) for nm in ("u", "v", "w", "p", "T")])
+            rt.periodic_fill([f["mx"], f["my"], f["mz"], f["E"]] + vel + [f["p"], f["T"]], 2, self.logical)
+            rt.par_loop(KernelHandle(K.NS_RHS_MASS, "ns_mass", K.NS_RHS_MASS, (self.inv12h, a, self.dt)), dom,
+                        [ArgSpec(U[1], S, R), ArgSpec(U[2], S, R), ArgSpec(U[3], S, R), ArgSpec(dU[0], P, RW)])
+            for c in range(3):
+                rt.par_loop(KernelHandle(K.NS_RHS_MOM + c, f"ns_mom{c}", K.NS_RHS_MOM + c,
+                                         (self.inv12h, self.inv12h2, self.mu, a, self.dt)), dom,
+                            [ArgSpec(U[1 + c], S, R)] + [ArgSpec(x, S, R) for x in vel] +
+                            [ArgSpec(f["p"], S, R), ArgSpec(dU[1 + c], P, RW)])
+            rt.par_loop(KernelHandle(K.NS_RHS_ENERGY, "ns_energy", K.NS_RHS_ENERGY,
+                                     (self.inv12h, self.inv12h2, self.mu, self.kappa, a, self.dt)), dom,
+                        [ArgSpec(U[4], S, R), ArgSpec(f["p"], S, R)] + [ArgSpec(x, S, R) for x in vel] +
+                        [ArgSpec(f["T"], S, R), ArgSpec(dU[4], P, RW)])
+            rt.par_loop(KernelHandle(K.NS_UPDATE, "ns_update", K.NS_UPDATE, (b,)), dom,
+                        [ArgSpec(x, P, RW) for x in U] + [ArgSpec(x, P, R) for x in dU])
+        return rt.par_loop(KernelHandle(K.NS_KINETIC, "ns_kinetic", K.NS_KINETIC), dom,
+                           [ArgSpec(x, P, R) for x in U[:4]], ReduceOp.Sum)
+
+    def cell_updates_per_step(self):
+        return 22 * self.n ** 3
+
+    def bytes_per_step(self):
+        # estimate_bytes_moved per loop (loop.cpp:50-61): 8 B per arg, x2 for RW.
+        per = 3 * ((5 + 5) + (3 + 2) + 3 * (5 + 2) + (6 + 2) + (10 + 5)) + 4
+        return 8 * per * self.n ** 3
+
+    def outputs(self):
+        return {nm: self.rt.download(self.f[nm]) for nm in ("rho", "mx", "my", "mz", "E")}

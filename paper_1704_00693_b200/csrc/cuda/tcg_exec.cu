@@ -148,6 +148,57 @@ __global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch
   }
 }
 
+// Periodic ghost fill along dimension D: for every field, the ghost layers
+// [L-depth, L) and [H, H+depth) in dim D take the values at +-N, over the
+// logical box in later dims and the ghost-extended box in earlier dims.
+constexpr int kMaxPeriodic = 16;
+struct PLaunch {
+  int32_t nf, depth;
+  int64_t L[3], H[3];
+  UArg f[kMaxPeriodic];
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) k_periodic(const __grid_constant__ PLaunch P) {
+  // Point grid over (2*depth) x ext(other dims), field index in blockIdx.y.
+  int64_t ext[3], org[3];
+  for (int d = 0; d < 3; ++d) {
+    if (d == D) {
+      ext[d] = 2 * P.depth;
+      org[d] = 0;
+    } else if (d < D) {
+      ext[d] = P.H[d] - P.L[d] + 2 * P.depth;
+      org[d] = P.L[d] - P.depth;
+    } else {
+      ext[d] = P.H[d] - P.L[d];
+      org[d] = P.L[d];
+    }
+  }
+  const int64_t total = ext[0] * ext[1] * ext[2];
+  const UArg& g = P.f[blockIdx.y];
+  const int64_t N = P.H[D] - P.L[D];
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t c[3];
+    c[0] = i % ext[0];
+    c[1] = (i / ext[0]) % ext[1];
+    c[2] = i / (ext[0] * ext[1]);
+    int64_t p[3];
+    for (int d = 0; d < 3; ++d) p[d] = org[d] + c[d];
+    int64_t s[3] = {p[0], p[1], p[2]};
+    if (c[D] < P.depth) {
+      p[D] = P.L[D] - P.depth + c[D];
+      s[D] = p[D] + N;
+    } else {
+      p[D] = P.H[D] + (c[D] - P.depth);
+      s[D] = p[D] - N;
+    }
+    double* dst = g.base + ((p[2] - g.z0) * g.pz + (p[1] - g.y0) * g.py + (p[0] - g.x0));
+    const double* src = g.base + ((s[2] - g.z0) * g.pz + (s[1] - g.y0) * g.py + (s[0] - g.x0));
+    *dst = *src;
+  }
+}
+
 }  // namespace
 
 
@@ -320,6 +371,60 @@ void DeviceExec::buf_to_field(int f, const Range& box, const double* buf, const 
                       buf_box.to_string());
   const BoxBuf fb{b->mem[b->cur], b->x0, lo_of(b->alloc, 1), lo_of(b->alloc, 2), b->py, b->ny};
   copy_box(fb, dense_buf(const_cast<double*>(buf), buf_box), box, static_cast<cudaStream_t>(stream_));
+}
+
+void DeviceExec::copy_within(int f, const Range& box, const Point& shift) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  Range src(box.dim());
+  for (int d = 0; d < box.dim(); ++d) src.set(d, box.start(d) + shift[d], box.end(d) + shift[d]);
+  if (!b->alloc.contains(box) || !b->alloc.contains(src))
+    throw AccessError("copy_within: " + box.to_string() + " / " + src.to_string() + " outside " + b->alloc.to_string());
+  if (box.empty()) return;
+  const BoxBuf fb{b->mem[b->cur], b->x0, lo_of(b->alloc, 1), lo_of(b->alloc, 2), b->py, b->ny};
+  cudaMemcpy3DParms p{};
+  p.srcPtr = p.dstPtr = make_cudaPitchedPtr(fb.base, static_cast<size_t>(fb.pitch) * 8, static_cast<size_t>(fb.pitch) * 8,
+                                            static_cast<size_t>(fb.rows));
+  p.srcPos = make_cudaPos(static_cast<size_t>(lo_of(src, 0) - fb.ox) * 8, static_cast<size_t>(lo_of(src, 1) - fb.oy),
+                          static_cast<size_t>(lo_of(src, 2) - fb.oz));
+  p.dstPos = make_cudaPos(static_cast<size_t>(lo_of(box, 0) - fb.ox) * 8, static_cast<size_t>(lo_of(box, 1) - fb.oy),
+                          static_cast<size_t>(lo_of(box, 2) - fb.oz));
+  p.extent = make_cudaExtent(static_cast<size_t>(ext_of(box, 0)) * 8, static_cast<size_t>(ext_of(box, 1)),
+                             static_cast<size_t>(ext_of(box, 2)));
+  p.kind = cudaMemcpyDeviceToDevice;
+  TCG_CK(cudaMemcpy3DAsync(&p, static_cast<cudaStream_t>(stream_)));
+}
+
+void DeviceExec::periodic_fill(const std::vector<int>& fields, const Range& logical, int64_t depth) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  const int dim = logical.dim();
+  for (size_t b = 0; b < fields.size(); b += kMaxPeriodic) {
+    PLaunch P{};
+    P.nf = static_cast<int32_t>(std::min<size_t>(kMaxPeriodic, fields.size() - b));
+    P.depth = static_cast<int32_t>(depth);
+    for (int d = 0; d < 3; ++d) {
+      P.L[d] = d < dim ? logical.start(d) : 0;
+      P.H[d] = d < dim ? logical.end(d) : 1;
+    }
+    for (int k = 0; k < P.nf; ++k) {
+      const DevView v = view(fields[b + static_cast<size_t>(k)], false);
+      P.f[k] = UArg{v.base, v.x0, v.y0, v.z0, v.py, v.pz, 0, 0};
+    }
+    for (int d = 0; d < dim; ++d) {
+      int64_t total = 2 * depth;
+      for (int e = 0; e < dim; ++e)
+        if (e != d) total *= (logical.extent(e) + (e < d ? 2 * depth : 0));
+      const dim3 grid(static_cast<unsigned>(std::min<int64_t>(4096, (total + 255) / 256)),
+                      static_cast<unsigned>(P.nf));
+      if (d == 0)
+        k_periodic<0><<<grid, 256, 0, st>>>(P);
+      else if (d == 1)
+        k_periodic<1><<<grid, 256, 0, st>>>(P);
+      else
+        k_periodic<2><<<grid, 256, 0, st>>>(P);
+      TCG_CK(cudaGetLastError());
+      ++launches_;
+    }
+  }
 }
 
 double* DeviceExec::staging(size_t n) {

@@ -71,6 +71,11 @@ class DeviceExec {
   // buffer laid out over buf_box (dim 0 fastest), host or device memory.
   void field_to_buf(int f, const Range& box, double* buf, const Range& buf_box);
   void buf_to_field(int f, const Range& box, const double* buf, const Range& buf_box);
+  // Copy box + shift -> box inside field f (periodic ghost layers).
+  void copy_within(int f, const Range& dst_box, const Point& shift);
+  // Periodic ghost fill of fields (all with the same logical box), all
+  // dimensions in order (edges/corners wrap), one kernel launch per dimension.
+  void periodic_fill(const std::vector<int>& fields, const Range& logical, int64_t depth);
   // Device staging for halo messages: >= n doubles, valid until the next
   // call that needs more.
   double* staging(size_t n);

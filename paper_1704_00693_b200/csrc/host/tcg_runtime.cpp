@@ -1279,6 +1279,29 @@ Range Runtime::local_box(DatasetId ds) {
   return h;
 }
 
+void Runtime::periodic_fill(const std::vector<DatasetId>& list, int64_t depth) {
+  flush();
+  if (distributed()) throw InvalidArgument("periodic_fill: not supported on a rank grid");
+  if (depth < 0) throw InvalidArgument("periodic_fill: negative depth");
+  ensure_fields();
+  // Group fields by logical box; one kernel per dimension per group.
+  std::vector<std::pair<Range, std::vector<int>>> groups;
+  for (DatasetId ds : list) {
+    const FieldRec& f = fields_.at(static_cast<size_t>(ds));
+    if (depth > f.pad) throw AccessError("periodic_fill: depth exceeds the pad of " + f.name);
+    for (int d = 0; d < dim_; ++d)
+      if (depth > f.logical.extent(d)) throw InvalidArgument("periodic_fill: depth exceeds the extent of " + f.name);
+    bool placed = false;
+    for (auto& g : groups)
+      if (g.first == f.logical) {
+        g.second.push_back(f.dev);
+        placed = true;
+      }
+    if (!placed) groups.emplace_back(f.logical, std::vector<int>{f.dev});
+  }
+  for (const auto& g : groups) device().periodic_fill(g.second, g.first, depth);
+}
+
 void Runtime::fill_logical(DatasetId ds, double v) {
   flush();
   const FieldRec& f = fields_.at(static_cast<size_t>(ds));

@@ -99,6 +99,11 @@ class Runtime {
   double get(DatasetId ds, const Point& p);
   void put(DatasetId ds, const Point& p, double v);
   void fill_logical(DatasetId ds, double v);
+  // Periodic boundary: copy the opposite side of the logical box into the
+  // ghost layers (depth <= pad) of every listed field, dimension by
+  // dimension so edges and corners wrap too. Flushes first. (The reference
+  // has no periodic support; c5 needs it.)
+  void periodic_fill(const std::vector<DatasetId>& ds, int64_t depth);
   // Bulk host <-> device copies of a whole allocation (dense, dim 0 fastest,
   // the reference Field layout, field.cpp:22-26). Flush first.
   void upload(DatasetId ds, const double* host);

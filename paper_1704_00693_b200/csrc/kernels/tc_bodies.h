@@ -166,6 +166,12 @@ TC_HD void hydro_loop(A& a, int kind, bool r3) {
   }
 }
 
+// Compile-time body tag (dispatch hands one to the executors' lambdas).
+template <int B>
+struct BodyTag {
+  static constexpr int value = B;
+};
+
 // ---------------------------------------------------------------------------
 // c5 compressible Navier-Stokes bodies live in their own header.
 }  // namespace tcb
@@ -200,11 +206,6 @@ TC_HD bool body_known(int32_t b) {
   X(kHydroBase + 4) X(kHydroBase + 5) X(kHydroBase + 6) X(kHydroBase + 7) X(kHydroBase + 8)             \
   X(kHydroBase + 9) X(kHydroCfl) X(kJacobi3D) X(kCgPUpdate) X(kCgMatvec) X(kCgXUpdate) X(kCgRUpdate)    \
   X(kCgDot)
-
-template <int B>
-struct BodyTag {
-  static constexpr int value = B;
-};
 
 // Calls f(BodyTag<body>{}) for a registered body; false if unknown.
 template <class F>

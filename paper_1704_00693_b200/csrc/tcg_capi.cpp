@@ -321,6 +321,10 @@ int tcg_local_box(tcg_runtime* rt, int32_t ds, int64_t out[6]) {
   });
 }
 
+int tcg_periodic_fill(tcg_runtime* rt, int n, const int32_t* ds, int64_t depth) {
+  return guard([&] { rt->rt->periodic_fill(std::vector<tcg::DatasetId>(ds, ds + n), depth); });
+}
+
 int tcg_rank_owned(tcg_runtime* rt, int32_t rank, int64_t out[6]) {
   return guard([&] {
     const tcg::RankLayout& lay = rt->rt->rank_layout();

@@ -25,7 +25,13 @@ CG_MATVEC = 401        # c4 q = A p, sum p.q
 CG_X_UPDATE = 402      # c4 x += alpha p
 CG_R_UPDATE = 403      # c4 r -= alpha q, sum r.r
 CG_DOT = 404           # c4 sum r.r
-NS_FIRST = 500         # c5 (3D compressible NS)
+NS_FIRST = 500         # c5 (3D compressible NS), csrc/kernels/tc_ns.h
+NS_PRIM = 500          # rho,mx,my,mz,E -> u,v,w,p,T        params [gamma-1]
+NS_RHS_MASS = 501      # dRho = a dRho + dt * RHS           params [1/12h, a, dt]
+NS_RHS_MOM = 502       # + component (0..2)                 params [1/12h, 1/12h^2, mu, a, dt]
+NS_RHS_ENERGY = 505    #                                    params [1/12h, 1/12h^2, mu, kappa, a, dt]
+NS_UPDATE = 506        # U += b dU                          params [b]
+NS_KINETIC = 507       # Sum 0.5 |m|^2 / rho
 
 
 def hydro_body(stencil_kind: int, has_r3: bool) -> int:

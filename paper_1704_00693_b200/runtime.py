@@ -103,6 +103,7 @@ def load_library() -> ctypes.CDLL:
                                                 ctypes.POINTER(_I64)]),
         "tcg_signature_pending": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
         "tcg_set_rank_grid": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
+        "tcg_periodic_fill": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I32), _I64]),
         "tcg_upload_box": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_I64)]),
         "tcg_download_box": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_I64)]),
         "tcg_local_box": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_I64)]),
@@ -425,6 +426,16 @@ class Runtime:
         out = np.empty(a.shape(), dtype=np.float64)
         _check(self._lib.tcg_download(self._h, ds, out.ctypes.data_as(_P)))
         return out
+
+    def periodic_fill(self, datasets, depth: int, logical=None) -> None:
+        """Periodic ghost layers (depth <= pad) for every listed field, over
+        each field's logical box (`logical`, if given, must equal it); flushes."""
+        ds = list(datasets)
+        if logical is not None:
+            for d in ds:
+                if list(self._logicals[d].lohi[: 2 * self.dim]) != list(logical)[: 2 * self.dim]:
+                    raise InvalidArgument("periodic_fill: box differs from the field's logical range")
+        _check(self._lib.tcg_periodic_fill(self._h, len(ds), _arr(_I32, ds), depth))
 
     def upload_box(self, ds: int, data: np.ndarray, box: Range) -> None:
         arr = np.ascontiguousarray(data, dtype=np.float64)

@@ -182,3 +182,23 @@ def test_empty_range_loops(oracle_lib, mode):
     got = C.run(Runtime(2), gc, mode)
     C.assert_same(got, want, "empty loops")
     assert float("inf") in [v for v, _ in got[1]]
+
+
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((0, 0, 0)), ExecMode.tiled((16, 16, 4)),
+                                  ExecMode.windowed(), ExecMode.tiled_auto()],
+                         ids=["untiled", "tiled", "tiled_ts", "windowed", "auto"])
+def test_ns_c5_matches_oracle(oracle_lib, mode):
+    # c5 (3D Navier-Stokes-like TGV, 22 loops/step incl. periodic ghost fills)
+    # at 16^3, 3 steps: conserved fields bit-exact, kinetic energy to 1e-12.
+    def run(rt):
+        rt.set_default_mode(mode)
+        c = configs.NsC5(rt, 16)
+        kes = [rt.fetch_reduction(c.enqueue_step()) for _ in range(3)]
+        return c.outputs(), kes
+
+    fo, ko = run(oracle_lib.OracleRuntime(3))
+    fg, kg = run(Runtime(3))
+    for k in fo:
+        assert np.array_equal(fg[k], fo[k]), k
+    for a, b in zip(kg, ko):
+        assert abs(a - b) <= 1e-12 * abs(b)

@@ -97,3 +97,20 @@ def test_reference_self_consistent_across_tile_sizes(ref_lib):
         want = C.run(ref_lib.RefRuntime(2), gc, ExecMode.untiled())
         got = C.run(ref_lib.RefRuntime(2, threads=3), gc, ExecMode.tiled(C.random_tile_sizes(seed, 2)))
         C.assert_same(got, want, f"seed{seed}")
+
+
+def test_oracle_matches_reference_ns_c5(ref_lib):
+    # c5 bodies (csrc/kernels/tc_ns.h) through the unmodified reference's
+    # KernelCtx vs the restatement; periodic ghosts by host copy.
+    def run(rt):
+        c = configs.NsC5(rt, 12)
+        kes = [rt.fetch_reduction(c.enqueue_step()) for _ in range(2)]
+        return c.outputs(), kes
+
+    import pyoracle
+
+    (fo, ko), (fr, kr) = run(pyoracle.OracleRuntime(3)), run(ref_lib.RefRuntime(3))
+    for k in fo:
+        assert np.array_equal(fo[k], fr[k]), k
+    assert ko == kr
+    assert all(np.isfinite(ko)) and ko[0] > 0
