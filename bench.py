@@ -324,8 +324,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=60.0)
     ap.add_argument("--shard", action="store_true", help="c2: use the sharded (NCCL) path even on one GPU")
     args = ap.parse_args()
-    # >= 3 per the contract; tiled_auto settles its executor choice in 6 flushes.
-    args.warmup = max(7, args.warmup)
+    # >= 3 per the contract; tiled_auto settles its executor choice in 9 flushes.
+    args.warmup = max(10, args.warmup)
 
     # tiled_auto's per-chain executor choices persist here, so a profiler run
     # of the same command (kernels serialised, timings distorted) executes

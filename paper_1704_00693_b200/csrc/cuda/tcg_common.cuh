@@ -70,7 +70,32 @@ size_t align_up(size_t v) {
   return (v + 255) / 256 * 256 + 0 * sizeof(T);
 }
 
-ChainDev upload_chain(const DevChain& ch, void* scratch, cudaStream_t st) {
+uint64_t fnv_bytes(uint64_t h, const void* p, size_t n) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+// Content hash of the chain tables upload_chain writes (loops, params,
+// stencil tables) plus the scratch address they go to.
+uint64_t chain_tables_hash(const DevChain& ch, const void* scratch) {
+  uint64_t h = 1469598103934665603ull;
+  h = fnv_bytes(h, &scratch, sizeof scratch);
+  h = fnv_bytes(h, ch.loops.data(), ch.loops.size() * sizeof(DevLoop));
+  h = fnv_bytes(h, ch.params.data(), ch.params.size() * sizeof(double));
+  h = fnv_bytes(h, ch.st_start.data(), ch.st_start.size() * 4);
+  h = fnv_bytes(h, ch.st_npts.data(), ch.st_npts.size() * 4);
+  h = fnv_bytes(h, ch.st_pts.data(), ch.st_pts.size() * 4);
+  return (h ^ ch.loops.size() * 31 ^ ch.params.size() * 131 ^ ch.st_pts.size() * 1031) | 1;
+}
+
+// Uploads the chain tables into scratch (skipped when *last_hash says the
+// scratch already holds identical tables: repeated flushes of one chain then
+// cost no host-to-device copies). Returns the device pointers.
+ChainDev upload_chain(const DevChain& ch, void* scratch, cudaStream_t st, uint64_t* last_hash = nullptr) {
+  const uint64_t hh = last_hash ? chain_tables_hash(ch, scratch) : 0;
+  const bool skip = last_hash && *last_hash == hh;
+  if (last_hash) *last_hash = hh;
   const size_t nl = ch.loops.size() * sizeof(DevLoop);
   const size_t np = std::max<size_t>(1, ch.params.size()) * sizeof(double);
   const size_t ns = std::max<size_t>(1, ch.st_start.size()) * 4;
@@ -79,20 +104,20 @@ ChainDev upload_chain(const DevChain& ch, void* scratch, cudaStream_t st) {
   size_t off = 0;
   ChainDev cd;
   cd.loops = reinterpret_cast<DevLoop*>(base + off);
-  if (nl) TCG_CK(cudaMemcpyAsync(base + off, ch.loops.data(), nl, cudaMemcpyHostToDevice, st));
+  if (nl && !skip) TCG_CK(cudaMemcpyAsync(base + off, ch.loops.data(), nl, cudaMemcpyHostToDevice, st));
   off += align_up<char>(nl);
   cd.params = reinterpret_cast<double*>(base + off);
-  if (!ch.params.empty())
+  if (!ch.params.empty() && !skip)
     TCG_CK(cudaMemcpyAsync(base + off, ch.params.data(), ch.params.size() * 8, cudaMemcpyHostToDevice, st));
   off += align_up<char>(np);
   int32_t* s0 = reinterpret_cast<int32_t*>(base + off);
-  if (!ch.st_start.empty()) TCG_CK(cudaMemcpyAsync(s0, ch.st_start.data(), ch.st_start.size() * 4, cudaMemcpyHostToDevice, st));
+  if (!ch.st_start.empty() && !skip) TCG_CK(cudaMemcpyAsync(s0, ch.st_start.data(), ch.st_start.size() * 4, cudaMemcpyHostToDevice, st));
   off += align_up<char>(ns);
   int32_t* s1 = reinterpret_cast<int32_t*>(base + off);
-  if (!ch.st_npts.empty()) TCG_CK(cudaMemcpyAsync(s1, ch.st_npts.data(), ch.st_npts.size() * 4, cudaMemcpyHostToDevice, st));
+  if (!ch.st_npts.empty() && !skip) TCG_CK(cudaMemcpyAsync(s1, ch.st_npts.data(), ch.st_npts.size() * 4, cudaMemcpyHostToDevice, st));
   off += align_up<char>(ns);
   int32_t* s2 = reinterpret_cast<int32_t*>(base + off);
-  if (!ch.st_pts.empty()) TCG_CK(cudaMemcpyAsync(s2, ch.st_pts.data(), ch.st_pts.size() * 4, cudaMemcpyHostToDevice, st));
+  if (!ch.st_pts.empty() && !skip) TCG_CK(cudaMemcpyAsync(s2, ch.st_pts.data(), ch.st_pts.size() * 4, cudaMemcpyHostToDevice, st));
   cd.st = DevStencils{s0, s1, s2};
   return cd;
 }

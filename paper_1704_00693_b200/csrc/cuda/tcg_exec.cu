@@ -40,7 +40,54 @@ struct ULaunch {
   double prm[kMaxParams];
   DevStencils st;
   double* partials;
+  // L2 prefetch of the block's read footprint (0 = off): union of the read
+  // stencils' offsets per dimension, and the mask of arguments that read.
+  int32_t pf, rmask;
+  int32_t rlo[3], rhi[3];
 };
+
+// Issues one bulk L2 prefetch (cp.async.bulk.prefetch.L2) per row segment of
+// the block's read footprint, for every reading argument, before any point
+// is computed: the block's DRAM misses are then all in flight at once
+// instead of one plane / row at a time behind the dependent loads (the 3D
+// walk was measured long-scoreboard bound at 46% occupancy).
+template <int DIM, int RUN>
+__device__ __forceinline__ void prefetch_footprint(const ULaunch& L) {
+  const int64_t xe = L.lo[0] + L.n[0], ye = L.lo[1] + L.n[1], ze = L.lo[2] + L.n[2];
+  const int64_t x0 = L.lo[0] + static_cast<int64_t>(blockIdx.x) * blockDim.x;
+  const int64_t x1 = min(x0 + static_cast<int64_t>(blockDim.x), xe);
+  int64_t y0, y1, z0, z1;
+  if (DIM == 2) {
+    y0 = L.lo[1] + static_cast<int64_t>(blockIdx.y) * blockDim.y * RUN;
+    y1 = min(y0 + static_cast<int64_t>(blockDim.y) * RUN, ye);
+    z0 = 0;
+    z1 = 1;
+  } else {
+    y0 = L.lo[1] + static_cast<int64_t>(blockIdx.y) * blockDim.y;
+    y1 = min(y0 + static_cast<int64_t>(blockDim.y), ye);
+    z0 = L.lo[2] + static_cast<int64_t>(blockIdx.z) * RUN;
+    z1 = min(z0 + static_cast<int64_t>(RUN), ze);
+  }
+  if (x0 >= x1 || y0 >= y1 || z0 >= z1) return;
+  const int64_t ex0 = x0 + L.rlo[0], ex1 = x1 + L.rhi[0];
+  const int64_t ey0 = y0 + L.rlo[1], ny = (y1 + L.rhi[1]) - ey0;
+  const int64_t ez0 = DIM == 3 ? z0 + L.rlo[2] : 0, nz = DIM == 3 ? (z1 + L.rhi[2]) - ez0 : 1;
+  const int rows = static_cast<int>(ny * nz);
+  const int nread = __popc(static_cast<unsigned>(L.rmask));
+  const int tid = threadIdx.x + blockDim.x * threadIdx.y, nth = blockDim.x * blockDim.y;
+  for (int i = tid; i < nread * rows; i += nth) {
+    const int k = i / rows, row = i - k * rows;
+    unsigned m = static_cast<unsigned>(L.rmask);
+    for (int j = 0; j < k; ++j) m &= m - 1;  // k-th reading argument
+    const UArg& g = L.a[__ffs(m) - 1];
+    const int64_t yy = ey0 + row % ny, zz = ez0 + row / ny;
+    const char* p0 = reinterpret_cast<const char*>(g.base + ((zz - g.z0) * g.pz + (yy - g.y0) * g.py + (ex0 - g.x0)));
+    const char* p1 = reinterpret_cast<const char*>(g.base + ((zz - g.z0) * g.pz + (yy - g.y0) * g.py + (ex1 - g.x0)));
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p0) & ~uintptr_t{15};
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p1) + 15) & ~uintptr_t{15};
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(static_cast<unsigned>(a1 - a0)) : "memory");
+  }
+}
 
 // Accessor over HBM. c[a] points at argument a's element for the current
 // point; a thread walks a short run of rows, advancing every pointer by one
@@ -95,6 +142,7 @@ struct GAcc {
 
 template <int DIM, int BODY, int kUntiledRun = 4>
 __global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch L) {
+  if (DIM >= 2 && L.pf) prefetch_footprint<DIM, kUntiledRun>(L);
   GAcc acc{L, {}, 0, 0, 0, red_identity(L.red_op)};
   if (DIM == 1) {
     acc.px = L.lo[0] + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -252,6 +300,7 @@ DeviceExec::~DeviceExec() {
   if (red_dev_) cudaFree(red_dev_);
   if (staging_) cudaFree(staging_);
   if (redbuf_) cudaFree(redbuf_);
+  drop_graphs();
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
 }
 
@@ -555,6 +604,7 @@ void* DeviceExec::ensure_scratch(size_t bytes) {
     }
     scratch_bytes_ = std::max(bytes, scratch_bytes_ * 2);
     TCG_CK(cudaMalloc(&scratch_, scratch_bytes_));
+    scratch_hash_ = 0;
   }
   return scratch_;
 }
@@ -571,12 +621,93 @@ double* DeviceExec::ensure_partials(size_t n) {
   return partials_;
 }
 
+namespace {
+// One untiled launch (a loop, or the fold of a reducing loop's partials).
+struct ULaunchRec {
+  ULaunch L;
+  const void* fn;
+  dim3 grid, block;
+  int64_t nblocks;
+  int red;  // >= 0: followed by k_fold into red_dev_[red]
+};
+
+uint64_t launch_key(const std::vector<ULaunchRec>& recs, int dim) {
+  // Structure of the launch sequence; loop parameters excluded (they are
+  // updated in place on a cached graph).
+  uint64_t h = fnv_bytes(1469598103934665603ull, &dim, sizeof dim);
+  for (const ULaunchRec& r : recs) {
+    ULaunch L = r.L;
+    std::memset(L.prm, 0, sizeof L.prm);
+    h = fnv_bytes(h, &L, sizeof L);
+    h = fnv_bytes(h, &r.fn, sizeof r.fn);
+    h = fnv_bytes(h, &r.grid, sizeof r.grid);
+    h = fnv_bytes(h, &r.block, sizeof r.block);
+    h = fnv_bytes(h, &r.red, sizeof r.red);
+  }
+  return h ^ recs.size();
+}
+}  // namespace
+
+// A chain's untiled launch sequence as one CUDA graph (built explicitly,
+// kernel nodes in loop order, k_fold after each reducing loop), replayed on
+// later flushes of the same structure; changed loop parameters (CG's alpha /
+// beta) are patched into the executable graph node by node.
+struct DeviceExec::UGraph {
+  uint64_t key = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphNode_t> nodes;  // kernel node per record
+  std::vector<ULaunch> launched;       // parameters the exec graph holds
+  int64_t kernels = 0;
+};
+
+void DeviceExec::drop_graphs() {
+  for (UGraph* g : graphs_) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+  }
+  graphs_.clear();
+}
+
 void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   void* scratch = ensure_scratch(chain_bytes(ch));
-  const ChainDev cd = upload_chain(ch, scratch, st);
+  const ChainDev cd = upload_chain(ch, scratch, st, &scratch_hash_);
+  // Block shape and rows per thread: TCG_UNTILED_CFG="bx,by,run" (2D) /
+  // TCG_UNTILED_CFG3 (3D) override the measured defaults (tuning).
+  static const int3 ucfg = [] {
+    // Measured on B200 (c2 4096^2, tools/sweep_untiled.sh): 256x1x4 best.
+    int3 c{256, 1, 4};
+    if (const char* e = std::getenv("TCG_UNTILED_CFG")) std::sscanf(e, "%d,%d,%d", &c.x, &c.y, &c.z);
+    if (c.x * c.y > 256 || c.x * c.y < 32 || (c.z != 2 && c.z != 4 && c.z != 8)) c = int3{256, 1, 4};
+    return c;
+  }();
+  static const int3 ucfg3 = [] {
+    // Measured on B200 (c3 512^3, tools/sweep3.sh): 64x2 with 8 planes per thread.
+    int3 c{64, 2, 8};
+    if (const char* e = std::getenv("TCG_UNTILED_CFG3")) std::sscanf(e, "%d,%d,%d", &c.x, &c.y, &c.z);
+    if (c.x * c.y > 256 || c.x * c.y < 32 || (c.z != 4 && c.z != 8)) c = int3{64, 2, 8};
+    return c;
+  }();
+  static const bool use_graphs = [] {
+    const char* e = std::getenv("TCG_GRAPHS");
+    return !e || std::atoi(e) != 0;
+  }();
+  static const bool prefetch = [] {
+    const char* e = std::getenv("TCG_PREFETCH_L2");
+    return !e || std::atoi(e) != 0;
+  }();
+  const int run2 = ch.dim == 2 ? ucfg.z : ch.dim == 3 ? ucfg3.z : 4;
+
+  // Lower every loop to a launch record.
+  std::vector<ULaunchRec> recs;
+  recs.reserve(ch.loops.size());
+  int64_t max_blocks = 0;
+  bool empty_red = false;
   for (const DevLoop& lp : ch.loops) {
-    ULaunch L{};
+    ULaunchRec R{};
+    ULaunch& L = R.L;
     L.body = lp.body;
     L.nargs = lp.nargs;
     L.red_op = lp.red >= 0 ? lp.red_op : 0;
@@ -601,83 +732,163 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
       L.a[a] = UArg{v.base, v.x0, v.y0, v.z0, v.py, v.pz, lp.args[a].mode, lp.args[a].stencil};
     }
     L.st = cd.st;
-    dim3 block, grid;
-    // Block shape and rows per thread (2D): TCG_UNTILED_CFG="bx,by,run"
-    // overrides the default 32x8x4 (tuning experiments).
-    static const int3 ucfg = [] {
-      // Measured on B200 (c2 4096^2, tools/sweep_untiled.sh): 256x1x4 best.
-      int3 c{256, 1, 4};
-      if (const char* e = std::getenv("TCG_UNTILED_CFG")) std::sscanf(e, "%d,%d,%d", &c.x, &c.y, &c.z);
-      if (c.x * c.y > 256 || c.x * c.y < 32 || (c.z != 2 && c.z != 4 && c.z != 8)) c = int3{256, 1, 4};
-      return c;
-    }();
-    static const int3 ucfg3 = [] {
-      // Measured on B200 (c3 512^3, tools/sweep3.sh): 64x2 with 8 planes per thread.
-      int3 c{64, 2, 8};
-      if (const char* e = std::getenv("TCG_UNTILED_CFG3")) std::sscanf(e, "%d,%d,%d", &c.x, &c.y, &c.z);
-      if (c.x * c.y > 256 || c.x * c.y < 32 || (c.z != 4 && c.z != 8)) c = int3{64, 2, 8};
-      return c;
-    }();
-    const int run2 = ch.dim == 2 ? ucfg.z : ch.dim == 3 ? ucfg3.z : 4;
-    if (ch.dim == 1) {
-      block = dim3(256, 1, 1);
-      grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + 255) / 256)), 1, 1);
-    } else if (ch.dim == 2) {
-      block = dim3(static_cast<unsigned>(ucfg.x), static_cast<unsigned>(ucfg.y), 1);
-      const int64_t ry = static_cast<int64_t>(ucfg.y) * run2;  // rows of y per block
-      grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + ucfg.x - 1) / ucfg.x)),
-                  static_cast<unsigned>(std::max<int64_t>(1, (n[1] + ry - 1) / ry)), 1);
-    } else {
-      block = dim3(static_cast<unsigned>(ucfg3.x), static_cast<unsigned>(ucfg3.y), 1);
-      grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + ucfg3.x - 1) / ucfg3.x)),
-                  static_cast<unsigned>(std::max<int64_t>(1, (n[1] + ucfg3.y - 1) / ucfg3.y)),
-                  static_cast<unsigned>(std::max<int64_t>(1, (n[2] + run2 - 1) / run2)));
+    L.pf = prefetch ? 1 : 0;
+    for (int a = 0; a < lp.nargs; ++a) {
+      if (lp.args[a].mode == tcb::kWrite) continue;
+      L.rmask |= 1 << a;
+      const int sid = lp.args[a].stencil;
+      const int s0 = ch.st_start[static_cast<size_t>(sid)], np = ch.st_npts[static_cast<size_t>(sid)];
+      for (int j = 0; j < np; ++j)
+        for (int d = 0; d < 3; ++d) {
+          L.rlo[d] = std::min(L.rlo[d], ch.st_pts[static_cast<size_t>(3 * (s0 + j) + d)]);
+          L.rhi[d] = std::max(L.rhi[d], ch.st_pts[static_cast<size_t>(3 * (s0 + j) + d)]);
+        }
     }
-    const int64_t nblocks = static_cast<int64_t>(grid.x) * grid.y * grid.z;
-    if (L.has_red) L.partials = ensure_partials(static_cast<size_t>(nblocks));
+    if (ch.dim == 1) {
+      R.block = dim3(256, 1, 1);
+      R.grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + 255) / 256)), 1, 1);
+    } else if (ch.dim == 2) {
+      R.block = dim3(static_cast<unsigned>(ucfg.x), static_cast<unsigned>(ucfg.y), 1);
+      const int64_t ry = static_cast<int64_t>(ucfg.y) * run2;  // rows of y per block
+      R.grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + ucfg.x - 1) / ucfg.x)),
+                    static_cast<unsigned>(std::max<int64_t>(1, (n[1] + ry - 1) / ry)), 1);
+    } else {
+      R.block = dim3(static_cast<unsigned>(ucfg3.x), static_cast<unsigned>(ucfg3.y), 1);
+      R.grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + ucfg3.x - 1) / ucfg3.x)),
+                    static_cast<unsigned>(std::max<int64_t>(1, (n[1] + ucfg3.y - 1) / ucfg3.y)),
+                    static_cast<unsigned>(std::max<int64_t>(1, (n[2] + run2 - 1) / run2)));
+    }
+    R.nblocks = static_cast<int64_t>(R.grid.x) * R.grid.y * R.grid.z;
+    R.red = L.has_red ? lp.red : -1;
     if (empty) {
       if (L.has_red) {
         // Empty reducing loop: the result is the identity.
         const double idv = red_identity(L.red_op);
         TCG_CK(cudaMemcpyAsync(red_dev_ + lp.red, &idv, 8, cudaMemcpyHostToDevice, st));
         TCG_CK(cudaStreamSynchronize(st));
+        empty_red = true;
       }
       continue;
-    }
-    void* e0 = nullptr;
-    if (timing_) {
-      e0 = take_event();
-      TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e0), st));
     }
     // One kernel instantiation per (dim, body): the body is a compile-time
     // constant inside the kernel.
     const bool known = tcb::dispatch(L.body, [&](auto tag) {
       constexpr int B = decltype(tag)::value;
       if (ch.dim == 1)
-        k_untiled<1, B><<<grid, block, 0, st>>>(L);
+        R.fn = reinterpret_cast<const void*>(k_untiled<1, B>);
       else if (ch.dim == 2 && run2 == 2)
-        k_untiled<2, B, 2><<<grid, block, 0, st>>>(L);
+        R.fn = reinterpret_cast<const void*>(k_untiled<2, B, 2>);
       else if (ch.dim == 2 && run2 == 8)
-        k_untiled<2, B, 8><<<grid, block, 0, st>>>(L);
+        R.fn = reinterpret_cast<const void*>(k_untiled<2, B, 8>);
       else if (ch.dim == 2)
-        k_untiled<2, B><<<grid, block, 0, st>>>(L);
+        R.fn = reinterpret_cast<const void*>(k_untiled<2, B>);
       else if (run2 == 8)
-        k_untiled<3, B, 8><<<grid, block, 0, st>>>(L);
+        R.fn = reinterpret_cast<const void*>(k_untiled<3, B, 8>);
       else
-        k_untiled<3, B><<<grid, block, 0, st>>>(L);
+        R.fn = reinterpret_cast<const void*>(k_untiled<3, B>);
     });
     if (!known) throw InvalidArgument("untiled executor: body " + std::to_string(L.body) + " not in the registry");
-    TCG_CK(cudaGetLastError());
-    if (timing_) {
-      void* e1 = take_event();
-      TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e1), st));
-      ev_untiled_.emplace_back(e0, e1);
+    if (L.has_red) max_blocks = std::max(max_blocks, R.nblocks);
+    recs.push_back(R);
+  }
+  // Reduction partials: one buffer region per reducing loop (a graph replays
+  // the loops back to back, so they must not share one).
+  if (max_blocks > 0) {
+    int64_t nr = 0;
+    for (const ULaunchRec& r : recs) nr += r.red >= 0 ? 1 : 0;
+    double* part = ensure_partials(static_cast<size_t>(max_blocks * nr));
+    int64_t i = 0;
+    for (ULaunchRec& r : recs)
+      if (r.red >= 0) r.L.partials = part + (i++) * max_blocks;
+  }
+
+  const bool graph_ok = use_graphs && !timing_ && !empty_red && !recs.empty();
+  if (graph_ok) {
+    const uint64_t key = launch_key(recs, ch.dim);
+    UGraph* g = nullptr;
+    for (UGraph* c : graphs_)
+      if (c->key == key) g = c;
+    if (!g) {
+      if (graphs_.size() >= 64) {
+        TCG_CK(cudaStreamSynchronize(st));
+        UGraph* old = graphs_.front();
+        cudaGraphExecDestroy(old->exec);
+        cudaGraphDestroy(old->graph);
+        delete old;
+        graphs_.erase(graphs_.begin());
+      }
+      g = new UGraph;
+      g->key = key;
+      TCG_CK(cudaGraphCreate(&g->graph, 0));
+      cudaGraphNode_t prev = nullptr;
+      for (ULaunchRec& r : recs) {
+        cudaKernelNodeParams kp{};
+        void* args[] = {&r.L};
+        kp.func = const_cast<void*>(r.fn);
+        kp.gridDim = r.grid;
+        kp.blockDim = r.block;
+        kp.kernelParams = args;
+        cudaGraphNode_t node;
+        TCG_CK(cudaGraphAddKernelNode(&node, g->graph, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+        g->nodes.push_back(node);
+        g->launched.push_back(r.L);
+        prev = node;
+        ++g->kernels;
+        if (r.red >= 0) {
+          const double* pp = r.L.partials;
+          int64_t nb = r.nblocks;
+          int op = r.L.red_op;
+          double* out = red_dev_ + r.red;
+          void* fargs[] = {&pp, &nb, &op, &out};
+          cudaKernelNodeParams fp{};
+          fp.func = reinterpret_cast<void*>(k_fold);
+          fp.gridDim = dim3(1);
+          fp.blockDim = dim3(1024);
+          fp.kernelParams = fargs;
+          cudaGraphNode_t fnode;
+          TCG_CK(cudaGraphAddKernelNode(&fnode, g->graph, &prev, 1, &fp));
+          prev = fnode;
+          ++g->kernels;
+        }
+      }
+      TCG_CK(cudaGraphInstantiate(&g->exec, g->graph, 0));
+      graphs_.push_back(g);
+    } else {
+      // Same structure: patch parameters that changed.
+      for (size_t i = 0; i < recs.size(); ++i) {
+        if (std::memcmp(recs[i].L.prm, g->launched[i].prm, sizeof recs[i].L.prm) == 0) continue;
+        cudaKernelNodeParams kp{};
+        void* args[] = {&recs[i].L};
+        kp.func = const_cast<void*>(recs[i].fn);
+        kp.gridDim = recs[i].grid;
+        kp.blockDim = recs[i].block;
+        kp.kernelParams = args;
+        TCG_CK(cudaGraphExecKernelNodeSetParams(g->exec, g->nodes[i], &kp));
+        g->launched[i] = recs[i].L;
+      }
     }
-    ++launches_;
-    if (L.has_red) {
-      k_fold<<<1, 1024, 0, st>>>(L.partials, nblocks, L.red_op, red_dev_ + lp.red);
-      TCG_CK(cudaGetLastError());
+    TCG_CK(cudaGraphLaunch(g->exec, st));
+    launches_ += g->kernels;
+  } else {
+    for (ULaunchRec& r : recs) {
+      void* e0 = nullptr;
+      if (timing_) {
+        e0 = take_event();
+        TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e0), st));
+      }
+      void* args[] = {&r.L};
+      TCG_CK(cudaLaunchKernel(r.fn, r.grid, r.block, args, 0, st));
+      if (timing_) {
+        void* e1 = take_event();
+        TCG_CK(cudaEventRecord(static_cast<cudaEvent_t>(e1), st));
+        ev_untiled_.emplace_back(e0, e1);
+      }
       ++launches_;
+      if (r.red >= 0) {
+        k_fold<<<1, 1024, 0, st>>>(r.L.partials, r.nblocks, r.L.red_op, red_dev_ + r.red);
+        TCG_CK(cudaGetLastError());
+        ++launches_;
+      }
     }
   }
   if (ch.nred > 0) {

@@ -332,7 +332,7 @@ void DeviceExec::run_l2(const DevChain& ch, const std::vector<DevItem>& items, c
   if (ch.loops.size() > static_cast<size_t>(kL2MaxLoops))
     throw PlanError("L2 tiled executor: more than 32 loops in one launch");
   void* scratch = ensure_scratch(chain_bytes(ch));
-  const ChainDev cd = upload_chain(ch, scratch, st);
+  const ChainDev cd = upload_chain(ch, scratch, st, &scratch_hash_);
   static L2Launch P;  // large (kernel parameters); host copy reused
   std::memset(&P, 0, sizeof P);
   for (size_t l = 0; l < ch.loops.size(); ++l) {

@@ -75,7 +75,7 @@ void DeviceExec::run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t 
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   PlanBufs* pb = plan_bufs(gp, key);
   void* scratch = ensure_scratch(chain_bytes(ch));
-  const ChainDev cd = upload_chain(ch, scratch, st);
+  const ChainDev cd = upload_chain(ch, scratch, st, &scratch_hash_);
   DevTiledPlan P{};
   P.dim = gp.dim;
   P.nloops = gp.nloops;

@@ -145,6 +145,10 @@ class DeviceExec {
   std::vector<ItemBufs> item_cache_;
   uint32_t epoch_ = 0;
   int64_t launches_ = 0;
+  uint64_t scratch_hash_ = 0;  // content hash of the chain tables in scratch_
+  struct UGraph;
+  std::vector<UGraph*> graphs_;  // untiled launch sequences as CUDA graphs
+  void drop_graphs();
   bool timing_ = false;
   std::vector<std::pair<void*, void*>> ev_tiled_, ev_untiled_;  // (start, stop) event pairs (k_l2tiled counts as tiled)
   std::vector<void*> ev_pool_;

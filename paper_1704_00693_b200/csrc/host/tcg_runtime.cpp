@@ -117,7 +117,7 @@ Runtime::Runtime(int dim, RuntimeConfig cfg) : dim_(dim), cfg_(cfg) {
         AutoStat& a = auto_[static_cast<uint64_t>(sig)];
         const float m[kCand] = {m0, m1, m2};
         for (int c = 0; c < kCand; ++c) {
-          a.runs[c] = 2;
+          a.runs[c] = kAutoRuns;
           a.ms[c] = m[c];
           a.fits[c] = ((fits >> c) & 1) != 0;
         }
@@ -392,9 +392,15 @@ void Runtime::run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionR
     return gp;
   };
 
+  // Upper bound on loops per windowed sub-chain (0 = as long as fits).
+  static const size_t max_loops = [] {
+    const char* e = std::getenv("TCG_WIN_MAXLOOPS");
+    return e ? static_cast<size_t>(std::max(0, std::atoi(e))) : size_t{0};
+  }();
   size_t begin = 0, red_base = 0;
   while (begin < chain.size()) {
     size_t len = chain.size() - begin;
+    if (max_loops > 0) len = std::min(len, max_loops);
     std::shared_ptr<const GpuTiledPlan> gp = plan_for(begin, len);
     if (!gp) {
       // Longest fitting prefix: fit is monotone in length for a fixed start.
@@ -747,7 +753,7 @@ std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode,
     cand = -1;
     if (!as->ev1) {
       for (int c = 0; c < kCand; ++c)
-        if (as->fits[c] && as->runs[c] < 2 && (cand < 0 || as->runs[c] < as->runs[cand])) cand = c;
+        if (as->fits[c] && as->runs[c] < kAutoRuns && (cand < 0 || as->runs[c] < as->runs[cand])) cand = c;
       measure = cand >= 0;
     }
     if (cand < 0) {
@@ -756,6 +762,7 @@ std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode,
     }
   }
   bool use_untiled = cand == 1;
+  if (measure) dev.synchronize();  // tuning only: time this chain alone, launch overhead included
   if (!use_untiled) {
     if (measure) as->ev0 = dev.record();
     try {

@@ -223,6 +223,7 @@ class Runtime {
   // tiled_auto: per chain signature, device time of each executor candidate
   // (0 L2-tiled, 1 untiled, 2 windowed); all bit-exact, the fastest is kept.
   static constexpr int kCand = 3;
+  static constexpr int kAutoRuns = 3;  // timed runs per candidate (min kept)
   struct AutoStat {
     int runs[kCand] = {0, 0, 0};
     float ms[kCand] = {1e30f, 1e30f, 1e30f};

@@ -10,9 +10,9 @@ from paper_1704_00693_b200 import Runtime  # noqa: E402
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 order = sys.argv[2].split(";") if len(sys.argv) > 2 else ["untiled", "auto", "untiled", "auto"]
-steps = 50
+steps = int(__import__("os").environ.get("AB_STEPS", "50"))
 for mname in order:
-    rt = Runtime(3 if cfg_name == "c3" else 2)
+    rt = Runtime(3 if cfg_name in ("c3", "c5") else 2)
     rt.set_default_mode(bench.parse_mode(mname))
     cfg = bench.make_config(cfg_name, rt)
     st = bench.Step(cfg_name, cfg, rt)
