@@ -300,6 +300,58 @@ def parse_report(text: str) -> dict:
     return rep
 
 
+class LazyReport(dict):
+    """ExecutionReport of one flush as key -> text value (ExecutionReport::
+    to_text keys, executor.cpp:321-366). The text is fetched when the flush
+    returns and parsed on first access, so a time-stepping loop that ignores
+    the report pays no parsing per step."""
+
+    def __init__(self, text: str):
+        super().__init__()
+        self._text = text
+
+    def _fill(self):
+        if self._text is not None:
+            t, self._text = self._text, None
+            super().update(parse_report(t))
+
+    def __getitem__(self, k):
+        self._fill()
+        return super().__getitem__(k)
+
+    def get(self, k, default=None):
+        self._fill()
+        return super().get(k, default)
+
+    def __contains__(self, k):
+        self._fill()
+        return super().__contains__(k)
+
+    def __iter__(self):
+        self._fill()
+        return super().__iter__()
+
+    def __len__(self):
+        self._fill()
+        return super().__len__()
+
+    def keys(self):
+        self._fill()
+        return super().keys()
+
+    def items(self):
+        self._fill()
+        return super().items()
+
+    def values(self):
+        self._fill()
+        return super().values()
+
+    def __repr__(self):
+        self._fill()
+        return super().__repr__()
+
+
 class Runtime:
     """tilechain::Runtime over the B200 executor."""
 
@@ -317,6 +369,7 @@ class Runtime:
         self._allocs: list[Range] = []
         self._logicals: list[Range] = []
         self._enc: dict = {}
+        self._rbuf = ctypes.create_string_buffer(1 << 14)
         self._out = _I32(-1)
         self._out_ref = ctypes.byref(self._out)
 
@@ -385,7 +438,7 @@ class Runtime:
             _check(self._lib.tcg_flush_default(self._h))
         else:
             _check(self._lib.tcg_flush(self._h, mode.kind, _arr(_I64, mode.tile_sizes)))
-        return parse_report(self.report_text())
+        return LazyReport(self.report_text())
 
     def set_default_mode(self, mode: ExecMode) -> None:
         _check(self._lib.tcg_set_default_mode(self._h, mode.kind, _arr(_I64, mode.tile_sizes)))
@@ -462,7 +515,16 @@ class Runtime:
 
     # ---- introspection ------------------------------------------------------
     def report_text(self) -> str:
-        return _text(self._lib.tcg_report_text, self._h)
+        # Idempotent call: start small (a per-flush 4 MiB buffer costs more
+        # host time than a small chain's whole device time) and retry.
+        need = _I64(0)
+        size = 1 << 14
+        while True:
+            buf = self._rbuf if size == 1 << 14 else ctypes.create_string_buffer(size)
+            _check(self._lib.tcg_report_text(self._h, buf, len(buf), ctypes.byref(need)))
+            if need.value <= size:
+                return buf.value.decode()
+            size = int(need.value) + 1
 
     def plan_pending(self, tile_sizes) -> str:
         ts = list(tile_sizes) + [0] * (3 - len(tile_sizes))
