@@ -289,11 +289,12 @@ TC_HD bool run_body(int32_t body, A& a, const double* p) {
     case kHydroCfl:
       a.contribute(0.5 / (a.read(0, 0, 0, 0) + a.read(1, 0, 0, 0) * a.read(2, 0, 0, 0)));
       return true;
-    // c3: b = 0.5*a + 0.5*(sum of 6 neighbours / 6)
+    // c3: b = 0.5*a + 0.5*(sum of 6 neighbours * 1/6) -- the 1/6 averaging
+    // coefficient is a constant product (no per-point IEEE division).
     case kJacobi3D: {
       const double s = ((((a.read(0, 1, 0, 0) + a.read(0, -1, 0, 0)) + a.read(0, 0, 1, 0)) +
                          a.read(0, 0, -1, 0)) + a.read(0, 0, 0, 1)) + a.read(0, 0, 0, -1);
-      a.write(1, 0.5 * a.read(0, 0, 0, 0) + 0.5 * (s / 6.0));
+      a.write(1, 0.5 * a.read(0, 0, 0, 0) + 0.5 * (s * (1.0 / 6.0)));
       return true;
     }
     // c4 CG. Args documented in DESIGN.md §configs.

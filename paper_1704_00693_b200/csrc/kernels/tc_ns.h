@@ -47,16 +47,18 @@ TC_HD double ns_at(const A& a, int arg, int axis, int k) {
 
 template <class A>
 TC_HD void ns_prim(A& a, const double* p) {
+  // One IEEE division per point (1/rho), products elsewhere.
   const double rho = a.read(0, 0, 0, 0);
-  const double u = a.read(1, 0, 0, 0) / rho;
-  const double v = a.read(2, 0, 0, 0) / rho;
-  const double w = a.read(3, 0, 0, 0) / rho;
+  const double rinv = 1.0 / rho;
+  const double u = a.read(1, 0, 0, 0) * rinv;
+  const double v = a.read(2, 0, 0, 0) * rinv;
+  const double w = a.read(3, 0, 0, 0) * rinv;
   const double pr = p[0] * (a.read(4, 0, 0, 0) - 0.5 * rho * ((u * u + v * v) + w * w));
   a.write(5, u);
   a.write(6, v);
   a.write(7, w);
   a.write(8, pr);
-  a.write(9, pr / rho);
+  a.write(9, pr * rinv);
 }
 
 template <class A>
