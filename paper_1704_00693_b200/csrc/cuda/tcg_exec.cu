@@ -140,8 +140,8 @@ struct GAcc {
 // Rows (2D: y, 3D: z) walked by one thread of the untiled executor
 // (template parameter kUntiledRun of k_untiled; 4 unless tuned).
 
-template <int DIM, int BODY, int kUntiledRun = 4>
-__global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch L) {
+template <int DIM, int BODY, int kUntiledRun>
+__device__ __forceinline__ void untiled_block(const ULaunch& L) {
   if (DIM >= 2 && L.pf) prefetch_footprint<DIM, kUntiledRun>(L);
   GAcc acc{L, {}, 0, 0, 0, red_identity(L.red_op)};
   if (DIM == 1) {
@@ -194,6 +194,18 @@ __global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch
     if (threadIdx.x == 0 && threadIdx.y == 0)
       L.partials[blockIdx.x + static_cast<int64_t>(gridDim.x) * (blockIdx.y + static_cast<int64_t>(gridDim.y) * blockIdx.z)] = v;
   }
+}
+
+// Register budget per dimension, measured on B200 (tools/ab_minb2.sh): the 2D
+// walk is DRAM-latency bound and gains from 6 resident blocks per SM (c2
+// -4%); the 3D walk spills and slows under any cap (c5 +20% at 4 blocks).
+template <int DIM, int BODY, int kUntiledRun = 4>
+__global__ void __launch_bounds__(256) k_untiled(const __grid_constant__ ULaunch L) {
+  untiled_block<DIM, BODY, kUntiledRun>(L);
+}
+template <int BODY, int kUntiledRun = 4>
+__global__ void __launch_bounds__(256, 6) k_untiled2(const __grid_constant__ ULaunch L) {
+  untiled_block<2, BODY, kUntiledRun>(L);
 }
 
 // Periodic ghost fill along dimension D: for every field, the ghost layers
@@ -777,11 +789,11 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
       if (ch.dim == 1)
         R.fn = reinterpret_cast<const void*>(k_untiled<1, B>);
       else if (ch.dim == 2 && run2 == 2)
-        R.fn = reinterpret_cast<const void*>(k_untiled<2, B, 2>);
+        R.fn = reinterpret_cast<const void*>(k_untiled2<B, 2>);
       else if (ch.dim == 2 && run2 == 8)
-        R.fn = reinterpret_cast<const void*>(k_untiled<2, B, 8>);
+        R.fn = reinterpret_cast<const void*>(k_untiled2<B, 8>);
       else if (ch.dim == 2)
-        R.fn = reinterpret_cast<const void*>(k_untiled<2, B>);
+        R.fn = reinterpret_cast<const void*>(k_untiled2<B>);
       else if (run2 == 8)
         R.fn = reinterpret_cast<const void*>(k_untiled<3, B, 8>);
       else

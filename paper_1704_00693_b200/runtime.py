@@ -25,7 +25,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_lib" / ("libtcg_debug.so" if __import__("os").environ.get("TCG_DEBUG_LIB") == "1" else "libtcg.so")
+LIB_PATH = Path(__import__("os").environ["TCG_LIB"]) if __import__("os").environ.get("TCG_LIB") else _PKG / "_lib" / ("libtcg_debug.so" if __import__("os").environ.get("TCG_DEBUG_LIB") == "1" else "libtcg.so")
 _lib: Optional[ctypes.CDLL] = None
 
 

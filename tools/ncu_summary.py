@@ -29,7 +29,9 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 
 def family(name: str) -> str:
     m = re.search(r"(k_\w+)", name)
-    return m.group(1) if m else name[:40]
+    if not m:
+        return name[:40]
+    return "k_untiled" if m.group(1) == "k_untiled2" else m.group(1)  # 2D instantiation, same executor
 
 
 def val(row, units, idx, m):
