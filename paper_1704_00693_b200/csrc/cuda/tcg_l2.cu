@@ -117,7 +117,7 @@ struct LAcc {
   __device__ __forceinline__ bool reduces() const { return L.red >= 0; }
 };
 
-constexpr int kRun = 4;  // rows (2D) / planes (3D) per thread
+constexpr int kRun = kL2Run;  // rows (2D) / planes (3D) per thread
 
 // Chunk extents per dimension (2D: 32 x 8 threads x kRun rows; 3D: 32 x 8
 // threads x kRun planes; 1D: 256).

@@ -10,6 +10,9 @@ namespace tcg {
 constexpr int kMaxArgs = 12;        // arguments per loop
 constexpr int kMaxChainDats = 32;   // distinct datasets per chain (tiled executor)
 constexpr int kMaxRed = 8;          // reducing loops per tiled chain
+// Rows (2D) / planes (3D) each thread of the L2-tiled executor walks per
+// chunk; chunks are 32 x 8*kL2Run (2D) and 32 x 8 x kL2Run (3D) points.
+constexpr int kL2Run = 4;  // 8 measured: c1 -7%, c3 -9%, c2 +18% (tools/ab_l2run.sh)
 
 // One dataset buffer on the device. Element (x, y, z) lives at
 // base[(z - z0) * pz + (y - y0) * py + (x - x0)], where x0 is a multiple of 16

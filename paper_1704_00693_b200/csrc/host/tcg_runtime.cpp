@@ -637,8 +637,8 @@ void Runtime::run_l2(const LoopChain& chain, const ExecMode& mode, ExecutionRepo
             di.lo[d] = d < chain.dim ? static_cast<int32_t>(r.start(d)) : 0;
             di.hi[d] = d < chain.dim ? static_cast<int32_t>(r.end(d)) : 1;
           }
-          // Chunk grid (matches k_l2tiled: 256 points in 1D, 32 x 32 in 2D,
-          // 32 x 8 x 4 in 3D).
+          // Chunk grid (matches k_l2tiled: 256 points in 1D, 32 x 8*kL2Run in 2D,
+          // 32 x 8 x kL2Run in 3D).
           const int64_t nx = r.extent(0);
           if (chain.dim == 1) {
             di.cx = static_cast<int32_t>((nx + 255) / 256);
@@ -646,12 +646,12 @@ void Runtime::run_l2(const LoopChain& chain, const ExecMode& mode, ExecutionRepo
             di.nch = di.cx;
           } else if (chain.dim == 2) {
             di.cx = static_cast<int32_t>((nx + 31) / 32);
-            di.cy = static_cast<int32_t>((r.extent(1) + 31) / 32);
+            di.cy = static_cast<int32_t>((r.extent(1) + 8 * kL2Run - 1) / (8 * kL2Run));
             di.nch = di.cx * di.cy;
           } else {
             di.cx = static_cast<int32_t>((nx + 31) / 32);
             di.cy = static_cast<int32_t>((r.extent(1) + 7) / 8);
-            di.nch = di.cx * di.cy * static_cast<int32_t>((r.extent(2) + 3) / 4);
+            di.nch = di.cx * di.cy * static_cast<int32_t>((r.extent(2) + kL2Run - 1) / kL2Run);
           }
           di.flag_off = flag_off;
           flag_off += di.nch;
