@@ -460,7 +460,7 @@ def main():
             if ds in boxes and boxes[ds] != rte.alloc_range(ds):
                 rte.download_box(ds, boxes[ds], out=out[ds])
             else:
-                out[ds][...] = rte.download(ds)
+                rte.download(ds, out=out[ds])
         rte.synchronize()
         dt = max_over_ranks(time.perf_counter() - t0, dist)
         nbytes = sum(host[ds].nbytes for ds in ids) * world

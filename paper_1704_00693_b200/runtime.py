@@ -474,9 +474,15 @@ class Runtime:
             raise InvalidArgument(f"upload: expected {a.volume()} values for {a}, got {arr.size}")
         _check(self._lib.tcg_upload(self._h, ds, arr.ctypes.data_as(_P)))
 
-    def download(self, ds: int) -> np.ndarray:
+    def download(self, ds: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Whole allocation, dense (dim 0 fastest). `out` (C-contiguous
+        float64 of the allocation's size; pinned memory copies at full
+        PCIe/C2C rate) is filled in place and returned."""
         a = self._allocs[ds]
-        out = np.empty(a.shape(), dtype=np.float64)
+        if out is None:
+            out = np.empty(a.shape(), dtype=np.float64)
+        elif out.dtype != np.float64 or not out.flags.c_contiguous or out.size != a.volume():
+            raise InvalidArgument(f"download: out must be C-contiguous float64 with {a.volume()} values")
         _check(self._lib.tcg_download(self._h, ds, out.ctypes.data_as(_P)))
         return out
 
