@@ -873,14 +873,16 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
   // Block shape and rows per thread: TCG_UNTILED_CFG="bx,by,run" (2D) /
   // TCG_UNTILED_CFG3 (3D) override the measured defaults (tuning).
   static const int3 ucfg = [] {
-    // Measured on B200 (c2 4096^2, tools/sweep_untiled.sh): 256x1x4 best.
-    int3 c{256, 1, 4};
+    // Measured on B200 (tools/ab_run.sh): 256x1 threads, 8 rows each (c2 -2%, c1 -4% vs 4 rows).
+    int3 c{256, 1, 8};
     if (const char* e = std::getenv("TCG_UNTILED_CFG")) std::sscanf(e, "%d,%d,%d", &c.x, &c.y, &c.z);
-    if (c.x * c.y > 256 || c.x * c.y < 32 || (c.z != 2 && c.z != 4 && c.z != 8)) c = int3{256, 1, 4};
+    if (c.x * c.y > 256 || c.x * c.y < 32 || (c.z != 2 && c.z != 4 && c.z != 8)) c = int3{256, 1, 8};
     return c;
   }();
+  // 3D: 64x2 threads; planes per thread chosen per loop (below) unless
+  // TCG_UNTILED_CFG3="bx,by,run" fixes them.
+  static const bool cfg3_env = std::getenv("TCG_UNTILED_CFG3") != nullptr;
   static const int3 ucfg3 = [] {
-    // Measured on B200 (c3 512^3, tools/sweep3.sh): 64x2 with 8 planes per thread.
     int3 c{64, 2, 8};
     if (const char* e = std::getenv("TCG_UNTILED_CFG3")) std::sscanf(e, "%d,%d,%d", &c.x, &c.y, &c.z);
     if (c.x * c.y > 256 || c.x * c.y < 32 || (c.z != 4 && c.z != 8)) c = int3{64, 2, 8};
@@ -909,7 +911,7 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
     const char* e = std::getenv("TCG_S3_ZR");
     return e ? std::max(1, std::atoi(e)) : 64;
   }();
-  const int run2 = ch.dim == 2 ? ucfg.z : ch.dim == 3 ? ucfg3.z : 4;
+  const int run_dim = ch.dim == 2 ? ucfg.z : ch.dim == 3 ? ucfg3.z : 4;
 
   // Lower every loop to a launch record.
   std::vector<ULaunchRec> recs;
@@ -944,6 +946,17 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
     }
     L.st = cd.st;
     L.pf = prefetch ? 1 : 0;
+    // Planes per thread in 3D: 8 for small stencils (c3's 7 points: the
+    // z-neighbours of 8 planes stay in registers), 4 when the loop reads
+    // more than 8 stencil points in total (c5's radius-2 RHS loops: 8 planes
+    // took 246-255 registers, 11% occupancy; measured c5 277 -> 257 ms).
+    int run2 = run_dim;
+    if (ch.dim == 3 && !cfg3_env) {
+      int pts = 0;
+      for (int a = 0; a < lp.nargs; ++a)
+        if (lp.args[a].mode != tcb::kWrite) pts += ch.st_npts[static_cast<size_t>(lp.args[a].stencil)];
+      run2 = pts <= 8 ? 8 : 4;
+    }
     for (int a = 0; a < lp.nargs; ++a) {
       if (lp.args[a].mode == tcb::kWrite) continue;
       L.rmask |= 1 << a;
