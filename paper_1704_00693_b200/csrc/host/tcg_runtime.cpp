@@ -765,21 +765,28 @@ std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode,
   // loop. Execute the non-empty ones only.
   std::vector<double> all_vals;
   std::vector<int> red_src;  // per reduction of `full`: index into vals, -1 = identity
-  LoopChain chain;
-  chain.dim = full.dim;
-  chain.stencils = full.stencils;
+  bool any_empty = false;
   {
     int nr = 0;
     for (const LoopRecord& lp : full.loops) {
       const bool empty = lp.range.empty();
+      any_empty = any_empty || empty;
       if (lp.reduction) {
         all_vals.push_back(reduce_identity(lp.reduction->op));
         red_src.push_back(empty ? -1 : nr);
         if (!empty) ++nr;
       }
-      if (!empty) chain.loops.push_back(lp);
     }
   }
+  // The non-empty loops (a copy only when some loop is empty).
+  LoopChain nonempty;
+  if (any_empty) {
+    nonempty.dim = full.dim;
+    nonempty.stencils = full.stencils;
+    for (const LoopRecord& lp : full.loops)
+      if (!lp.range.empty()) nonempty.loops.push_back(lp);
+  }
+  const LoopChain& chain = any_empty ? nonempty : full;
   if (chain.loops.empty()) return all_vals;
   size_t nred = 0;
   for (const LoopRecord& lp : chain.loops) nred += lp.reduction ? 1 : 0;

@@ -417,20 +417,25 @@ class Runtime:
     def par_loop(self, kernel: KernelHandle, rng: Range, args: Sequence, reduction: Optional[int] = None) -> int:
         if rng.dim != self.dim:
             raise InvalidArgument("par_loop: range dim does not match block")
-        # Encoded ctypes arguments are cached per (range, args, params): a
-        # time-stepping code re-enqueues the same loops every step.
+        # Encoded ctypes arguments are cached per (range, args): a
+        # time-stepping code re-enqueues the same loops every step. Scalar
+        # parameters change from step to step (CG's alpha / beta) and are
+        # encoded per call.
         key = (tuple(rng.lohi), tuple((a.dataset, a.stencil, int(a.mode)) if isinstance(a, ArgSpec)
-                                      else (int(a[0]), int(a[1]), int(a[2])) for a in args), tuple(kernel.params))
+                                      else (int(a[0]), int(a[1]), int(a[2])) for a in args))
         enc = self._enc.get(key)
         if enc is None:
             flat = [v for t in key[1] for v in t]
-            enc = (_arr(_I64, key[0]), len(key[1]), _arr(_I32, flat), len(key[2]), _arr(_D, key[2]))
+            enc = (_arr(_I64, key[0]), len(key[1]), _arr(_I32, flat))
             if len(self._enc) > 4096:
                 self._enc.clear()
             self._enc[key] = enc
+        prm = kernel.params
+        np_ = len(prm)
         out = self._out
         _check(self._lib.tcg_par_loop(self._h, kernel.id, kernel.body, enc[0], enc[1], enc[2],
-                                      -1 if reduction is None else int(reduction), enc[3], enc[4], self._out_ref))
+                                      -1 if reduction is None else int(reduction), np_,
+                                      (_D * np_)(*prm) if np_ else None, self._out_ref))
         return out.value
 
     def flush(self, mode: Optional[ExecMode] = None) -> dict:
