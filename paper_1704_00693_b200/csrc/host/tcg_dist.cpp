@@ -44,6 +44,14 @@ DistSchedule build_dist_schedule(const LoopChain& chain, const RankLayout& layou
     }
     w.spec = compute_halo_depths(plan, chain, layout, r, prior);
   }
+  build_messages(s, layout, pads);
+  return s;
+}
+
+void build_messages(DistSchedule& s, const RankLayout& layout, const std::vector<int64_t>& pads) {
+  const int R = layout.rank_count();
+  s.msgs.clear();
+  s.message_bytes = 0;
   // exchange_halos (dist.cpp:463-511): dimension-ordered; strips of dims
   // already exchanged are widened by the receiver's depth there, so corners
   // arrive through the neighbour.
@@ -99,7 +107,64 @@ DistSchedule build_dist_schedule(const LoopChain& chain, const RankLayout& layou
     }
   }
   for (int d = layout.dim; d <= kMaxDims; ++d) s.phase[static_cast<size_t>(d)] = s.msgs.size();
-  return s;
+}
+
+std::vector<DistSchedule> build_untiled_schedules(const LoopChain& chain, const RankLayout& layout,
+                                                  const std::vector<int64_t>& pads) {
+  // DistContext::run_untiled (dist.cpp:691-788): per loop, exchange exactly
+  // the faces this loop reads that are stale (every face of a dataset goes
+  // stale when any loop writes it; nothing is fresh at chain start), then
+  // every rank runs the loop over its owned part.
+  const int R = layout.rank_count();
+  std::vector<DistSchedule> out;
+  out.reserve(chain.size());
+  std::map<DatasetId, std::array<HaloSpec::Faces, kMaxDims>> valid;
+  for (const LoopRecord& loop : chain.loops) {
+    HaloSpec spec;
+    for (const ArgSpec& a : loop.args) {
+      if (!mode_reads(a.mode)) continue;
+      const Stencil& st = chain.stencil(a.stencil);
+      auto& have = valid[a.dataset];
+      HaloSpec::Entry e;
+      bool stale = false;
+      for (int d = 0; d < chain.dim; ++d) {
+        e.faces[static_cast<size_t>(d)].lo = std::max<int64_t>(0, -st.min_offset(d));
+        e.faces[static_cast<size_t>(d)].hi = std::max<int64_t>(0, st.max_offset(d));
+        stale = stale || e.faces[static_cast<size_t>(d)].lo > have[static_cast<size_t>(d)].lo ||
+                e.faces[static_cast<size_t>(d)].hi > have[static_cast<size_t>(d)].hi;
+      }
+      if (!stale) continue;
+      e.needed = true;
+      auto [it, inserted] = spec.entries.emplace(a.dataset, e);
+      if (!inserted)
+        for (int d = 0; d < chain.dim; ++d) {
+          auto& f = it->second.faces[static_cast<size_t>(d)];
+          f.lo = std::max(f.lo, e.faces[static_cast<size_t>(d)].lo);
+          f.hi = std::max(f.hi, e.faces[static_cast<size_t>(d)].hi);
+        }
+    }
+    for (const auto& [ds, e] : spec.entries) {
+      auto& have = valid[ds];
+      for (int d = 0; d < chain.dim; ++d) {
+        have[static_cast<size_t>(d)].lo = std::max(have[static_cast<size_t>(d)].lo, e.faces[static_cast<size_t>(d)].lo);
+        have[static_cast<size_t>(d)].hi = std::max(have[static_cast<size_t>(d)].hi, e.faces[static_cast<size_t>(d)].hi);
+      }
+    }
+    DistSchedule s;
+    s.ranks.resize(static_cast<size_t>(R));
+    for (int r = 0; r < R; ++r) {
+      RankWork& w = s.ranks[static_cast<size_t>(r)];
+      w.owned = layout.owned[static_cast<size_t>(r)];
+      w.loop_ranges.push_back(loop.range.intersect(w.owned));
+      w.computed_points = w.loop_ranges.back().volume();
+      w.spec = spec;
+    }
+    build_messages(s, layout, pads);
+    out.push_back(std::move(s));
+    for (const ArgSpec& a : loop.args)
+      if (mode_writes(a.mode)) valid[a.dataset] = {};
+  }
+  return out;
 }
 
 bool note_writes(WriteHistory& hist, const LoopChain& chain) {

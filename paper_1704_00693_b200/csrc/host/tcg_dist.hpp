@@ -56,6 +56,16 @@ Range rank_alloc(const RankLayout& layout, int rank, int64_t pad);
 DistSchedule build_dist_schedule(const LoopChain& chain, const RankLayout& layout,
                                  const std::vector<int64_t>& pads, const WriteHistory* prior);
 
+// Halo messages of s.ranks[*].spec (exchange_halos order, dist.cpp:463-511).
+void build_messages(DistSchedule& s, const RankLayout& layout, const std::vector<int64_t>& pads);
+
+// On-demand untiled distribution (DistContext::run_untiled, dist.cpp:691-788):
+// one schedule per loop -- the stale faces that loop reads, exchanged just
+// before it; every rank then runs the loop over its owned part. The baseline
+// that the deep-halo schedule's "fewer, larger messages" is measured against.
+std::vector<DistSchedule> build_untiled_schedules(const LoopChain& chain, const RankLayout& layout,
+                                                  const std::vector<int64_t>& pads);
+
 // note_writes (dist.cpp:590-602): remember every written loop range that is
 // not already held by a recorded box. Returns true when the history changed.
 bool note_writes(WriteHistory& hist, const LoopChain& chain);

@@ -1100,15 +1100,18 @@ void Runtime::exchange(const DistSchedule& s, ExecutionReport& rep) {
       dev.buf_to_field(t.dev[static_cast<size_t>(m.ds)], m.box, stg + off[i - a], m.box);
     }
   }
-  rep.halo_messages = static_cast<int64_t>(s.msgs.size());
-  rep.halo_bytes = s.message_bytes;
-  rep.halo_exchanges = s.msgs.empty() ? 0 : 1;
+  rep.halo_messages += static_cast<int64_t>(s.msgs.size());
+  rep.halo_bytes += s.message_bytes;
+  rep.halo_exchanges += s.msgs.empty() ? 0 : 1;
 }
 
 ExecutionReport Runtime::execute_distributed(LoopChain chain, const ExecMode& mode) {
-  // DistContext::run_tiled (dist.cpp:617-689): plans + halo specs for every
-  // rank, one exchange, per-rank execution with reductions masked to the
-  // owned box, rank-order fold, note_writes.
+  // Tiled modes: DistContext::run_tiled (dist.cpp:617-689) -- plans + halo
+  // specs for every rank, ONE deep-halo exchange, per-rank execution of the
+  // rank-local chain with reductions masked to the owned box, rank-order
+  // fold, note_writes. Untiled: DistContext::run_untiled (dist.cpp:691-788)
+  // -- per loop, an on-demand exchange of the stale faces it reads, then the
+  // loop on every rank's owned part (the message-count baseline).
   const auto t0 = std::chrono::steady_clock::now();
   ExecutionReport rep;
   rep.dim = chain.dim;
@@ -1118,8 +1121,23 @@ ExecutionReport Runtime::execute_distributed(LoopChain chain, const ExecMode& mo
   ensure_dist();
   DeviceExec& dev = device();
   const int64_t l0 = dev.launches();
-  const auto sched = dist_schedule(chain);
-  exchange(*sched, rep);
+  const bool on_demand = mode.kind == ExecMode::Kind::Untiled;
+  // Stages: (schedule, loops [begin, end) of the chain it covers).
+  std::vector<std::shared_ptr<const DistSchedule>> stages;
+  if (on_demand) {
+    auto it = dist_->untiled_schedules.find(chain.signature());
+    if (it == dist_->untiled_schedules.end()) {
+      std::vector<int64_t> pads;
+      for (const FieldRec& f : fields_) pads.push_back(f.pad);
+      std::vector<std::shared_ptr<const DistSchedule>> v;
+      for (DistSchedule& s : build_untiled_schedules(chain, dist_->layout, pads))
+        v.push_back(std::make_shared<const DistSchedule>(std::move(s)));
+      it = dist_->untiled_schedules.emplace(chain.signature(), std::move(v)).first;
+    }
+    stages = it->second;
+  } else {
+    stages.push_back(dist_schedule(chain));
+  }
   const std::vector<ReductionHandle> handles = reduction_handles(chain);
   std::vector<ReduceOp> ops;
   for (const LoopRecord& lp : chain.loops)
@@ -1128,25 +1146,41 @@ ExecutionReport Runtime::execute_distributed(LoopChain chain, const ExecMode& mo
   const int R = dist_->layout.rank_count();
   std::vector<double> part(static_cast<size_t>(R) * nred, 0.0);
   std::string executor;
-  for (int r : dist_->local) {
-    const LoopChain lc = with_ranges(chain, sched->ranks[static_cast<size_t>(r)].loop_ranges);
-    ExecutionReport rr;
-    rr.dim = chain.dim;
-    const std::vector<double> v = run_on(lc, mode, rr, dist_->targets[static_cast<size_t>(r)]);
-    for (size_t i = 0; i < nred; ++i) part[static_cast<size_t>(r) * nred + i] = v[i];
-    rep.tiled = rep.tiled || rr.tiled;
-    executor = executor.empty() || executor == rr.executor ? rr.executor : "mixed";
-    rep.ctas += rr.ctas;
-    rep.subchains += rr.subchains;
-    rep.tiles_executed += rr.tiles_executed;
-    rep.plan_constructions += rr.plan_constructions;
-    rep.plan_seconds += rr.plan_seconds;
-    rep.computed_points += rr.tiled ? rr.computed_points : sched->ranks[static_cast<size_t>(r)].computed_points;
-    for (int d = 0; d < chain.dim; ++d) {
-      rep.max_skew[d] = std::max(rep.max_skew[d], rr.max_skew[d]);
-      rep.tile_sizes[d] = rr.tile_sizes[d];
-      rep.cta_grid[d] = rr.cta_grid[d];
+  size_t red_base = 0;
+  for (size_t st = 0; st < stages.size(); ++st) {
+    const DistSchedule& sched = *stages[st];
+    // The loops this stage runs: the whole chain, or loop `st` alone.
+    LoopChain sub;
+    if (on_demand) {
+      sub.dim = chain.dim;
+      sub.stencils = chain.stencils;
+      sub.loops.push_back(chain.loops[st]);
     }
+    const LoopChain& sc = on_demand ? sub : chain;
+    size_t sub_red = 0;
+    for (const LoopRecord& lp : sc.loops) sub_red += lp.reduction ? 1 : 0;
+    exchange(sched, rep);
+    for (int r : dist_->local) {
+      const LoopChain lc = with_ranges(sc, sched.ranks[static_cast<size_t>(r)].loop_ranges);
+      ExecutionReport rr;
+      rr.dim = chain.dim;
+      const std::vector<double> v = run_on(lc, mode, rr, dist_->targets[static_cast<size_t>(r)]);
+      for (size_t i = 0; i < sub_red; ++i) part[static_cast<size_t>(r) * nred + red_base + i] = v[i];
+      rep.tiled = rep.tiled || rr.tiled;
+      executor = executor.empty() || executor == rr.executor ? rr.executor : "mixed";
+      rep.ctas += rr.ctas;
+      rep.subchains += rr.subchains;
+      rep.tiles_executed += rr.tiles_executed;
+      rep.plan_constructions += rr.plan_constructions;
+      rep.plan_seconds += rr.plan_seconds;
+      rep.computed_points += rr.tiled ? rr.computed_points : sched.ranks[static_cast<size_t>(r)].computed_points;
+      for (int d = 0; d < chain.dim; ++d) {
+        rep.max_skew[d] = std::max(rep.max_skew[d], rr.max_skew[d]);
+        rep.tile_sizes[d] = rr.tile_sizes[d];
+        rep.cta_grid[d] = rr.cta_grid[d];
+      }
+    }
+    red_base += sub_red;
   }
   rep.executor = executor;
   if (comm_ && nred > 0) {

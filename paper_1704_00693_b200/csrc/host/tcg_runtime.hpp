@@ -173,6 +173,8 @@ class Runtime {
     WriteHistory written;              // note_writes history (dist.cpp:590-602)
     uint64_t hist_version = 0;
     std::map<std::pair<uint64_t, uint64_t>, std::shared_ptr<const DistSchedule>> schedules;
+    // Untiled (on-demand) per-loop schedules, per chain signature.
+    std::map<uint64_t, std::vector<std::shared_ptr<const DistSchedule>>> untiled_schedules;
   };
 
   ExecutionReport execute_chain(LoopChain chain, const ExecMode& mode);

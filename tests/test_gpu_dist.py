@@ -115,3 +115,34 @@ def test_process_rank_single_process_nccl():
     want = [ref.fetch_reduction(hr.enqueue_step()) for _ in range(2)]
     assert mins == want
     assert rt.get(h.d[0], (3, 3)) == ref.get(hr.d[0], (3, 3))
+
+
+@pytest.mark.parametrize("grid", [(1, 2, 1), (2, 2, 1)])
+def test_untiled_on_demand_exchange_matches_reference(ref_lib, grid):
+    # DistContext::run_untiled (dist.cpp:691-788): a halo exchange before each
+    # loop that reads stale faces. Same fields and the same message count and
+    # bytes as the reference's own simulated ranks; the deep-halo (tiled)
+    # schedule moves the chain's halos in one exchange of fewer, larger
+    # messages (acceptance.cpp:348-386).
+    steps = 5
+    ref = ref_lib.RefRuntime(2)
+    ref.set_rank_grid(grid)
+    hr = configs.HeatC1(ref, 64)
+    hr.enqueue_chain(steps=steps)
+    rep_ref = ref.flush(ExecMode.untiled())
+    rt = _GridRuntime(2, grid)
+    hg = configs.HeatC1(rt, 64)
+    hg.enqueue_chain(steps=steps)
+    rep = rt.flush(ExecMode.untiled())
+    assert int(rep["halo_messages"]) == int(rep_ref["halo_messages"]) > 0
+    assert int(rep["halo_bytes"]) == int(rep_ref["halo_bytes"])
+    assert int(rep["halo_exchanges"]) == steps  # one per Laplacian loop; the copies read at a point
+    assert np.array_equal(hg.outputs()["u"], hr.outputs()["u"])
+    # Deep halo on a fresh pair of runtimes: one exchange, fewer messages.
+    rt2 = _GridRuntime(2, grid)
+    h2 = configs.HeatC1(rt2, 64)
+    h2.enqueue_chain(steps=steps)
+    rep2 = rt2.flush(ExecMode.tiled((0, 0, 0)))
+    assert int(rep2["halo_exchanges"]) == 1
+    assert int(rep2["halo_messages"]) * steps == int(rep["halo_messages"])
+    assert np.array_equal(h2.outputs()["u"], hr.outputs()["u"])
