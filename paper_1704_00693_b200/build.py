@@ -20,6 +20,7 @@ LIB_DIR = PKG / "_lib"
 DEBUG = os.environ.get("TCG_DEBUG_BUILD") == "1"  # device printf diagnostics, separate .so
 OBJ_DIR = LIB_DIR / ("obj_debug" if DEBUG else "obj")
 LIB = LIB_DIR / ("libtcg_debug.so" if DEBUG else "libtcg.so")
+LIB_CHECKED = LIB_DIR / "libtcg_checked.so"
 REPO = PKG.parent
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -76,13 +77,26 @@ def build(verbose: bool = False) -> Path:
         objs.append(obj)
         if _stale(obj, src, headers):
             jobs.append(([NVCC, *NVCCFLAGS, "-c", str(src), "-o", str(obj)], obj.with_suffix(".log")))
-    if jobs:
-        with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
-            for f in [ex.submit(_compile, c, l) for c, l in jobs]:
+    # Checked variant (libtcg_checked.so): the untiled executor with the
+    # reference's KernelCtx access checks on the device (-DTCG_CHECKED); the
+    # other objects are shared.
+    src = CSRC / "cuda/tcg_exec.cu"
+    cobj = OBJ_DIR / "cuda_tcg_exec.cu.checked.o"
+    checked_jobs = []
+    if _stale(cobj, src, headers):
+        checked_jobs.append(([NVCC, *NVCCFLAGS, "-DTCG_CHECKED", "-c", str(src), "-o", str(cobj)],
+                             cobj.with_suffix(".log")))
+    if jobs or checked_jobs:
+        allj = jobs + checked_jobs
+        with cf.ThreadPoolExecutor(max_workers=min(8, len(allj))) as ex:
+            for f in [ex.submit(_compile, c, l) for c, l in allj]:
                 f.result()
     if jobs or not LIB.exists():
         cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcuda", "-ldl"]
         _compile(cmd, LIB_DIR / "link.log")
+    if jobs or checked_jobs or not LIB_CHECKED.exists():
+        cobjs = [str(cobj) if o.name == "cuda_tcg_exec.cu.o" else str(o) for o in objs]
+        _compile([NVCC, *ARCH, "-shared", "-o", str(LIB_CHECKED), *cobjs, "-lcuda", "-ldl"], LIB_DIR / "link_checked.log")
     if verbose:
         print(f"built {LIB}")
     return LIB

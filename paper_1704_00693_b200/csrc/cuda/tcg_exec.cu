@@ -48,7 +48,43 @@ struct ULaunch {
   // shared-memory ring base (doubles) of each reading argument.
   int32_t sty, szr, sslots, pad3_;
   int32_t sring[kMaxArgs];
+#ifdef TCG_CHECKED
+  int64_t alo[kMaxArgs][3], ahi[kMaxArgs][3];  // allocation of each argument
+#endif
 };
+
+#ifdef TCG_CHECKED
+// Checked build (libtcg_checked.so): the reference's KernelCtx checks
+// (kernel_ctx.hpp:58-89) on the device -- access mode, stencil membership of
+// every read offset, allocation bounds -- reported and trapped.
+__device__ __noinline__ void checked_fail(const ULaunch& L, int a, int dx, int dy, int dz, int64_t x, int64_t y,
+                                          int64_t z, const char* what) {
+  printf("tcg checked: body %d arg %d offset (%d,%d,%d) at point (%lld,%lld,%lld): %s\n", L.body, a, dx, dy, dz,
+         static_cast<long long>(x), static_cast<long long>(y), static_cast<long long>(z), what);
+  __trap();
+}
+__device__ __noinline__ void checked_access(const ULaunch& L, int a, int dx, int dy, int dz, int64_t x, int64_t y,
+                                            int64_t z, bool rd, bool wr) {
+  if (a < 0 || a >= L.nargs) checked_fail(L, a, dx, dy, dz, x, y, z, "argument index out of range");
+  const int m = L.a[a].mode;
+  if (rd && m == tcb::kWrite) checked_fail(L, a, dx, dy, dz, x, y, z, "read of a Write-mode argument");
+  if (wr && m == tcb::kRead) checked_fail(L, a, dx, dy, dz, x, y, z, "write of a Read-mode argument");
+  if (rd) {
+    const int s = L.a[a].stencil, n = L.st.npts[s], b = L.st.start[s];
+    bool found = false;
+    for (int j = 0; j < n && !found; ++j)
+      found = L.st.pts[3 * (b + j)] == dx && L.st.pts[3 * (b + j) + 1] == dy && L.st.pts[3 * (b + j) + 2] == dz;
+    if (!found) checked_fail(L, a, dx, dy, dz, x, y, z, "offset is not a point of the argument's stencil");
+  }
+  const int64_t p[3] = {x + dx, y + dy, z + dz};
+  for (int d = 0; d < 3; ++d)
+    if (p[d] < L.alo[a][d] || p[d] >= L.ahi[a][d])
+      checked_fail(L, a, dx, dy, dz, x, y, z, "access outside the allocated extent");
+}
+#define TCG_CHECK_ACCESS(a, dx, dy, dz, rd, wr) checked_access(L, a, dx, dy, dz, px, py, pz, rd, wr)
+#else
+#define TCG_CHECK_ACCESS(a, dx, dy, dz, rd, wr) ((void)0)
+#endif
 
 // Issues one bulk L2 prefetch (cp.async.bulk.prefetch.L2) per row segment of
 // the block's read footprint, for every reading argument, before any point
@@ -123,9 +159,18 @@ struct GAcc {
   __device__ __forceinline__ int64_t x() const { return px; }
   __device__ __forceinline__ int64_t y() const { return py; }
   __device__ __forceinline__ int64_t z() const { return pz; }
-  __device__ __forceinline__ double read(int a, int dx, int dy, int dz) const { return __ldg(at(a, dx, dy, dz)); }
-  __device__ __forceinline__ void write(int a, double v) const { *c[a] = v; }
-  __device__ __forceinline__ void increment(int a, double v) const { *c[a] = __ldg(c[a]) + v; }
+  __device__ __forceinline__ double read(int a, int dx, int dy, int dz) const {
+    TCG_CHECK_ACCESS(a, dx, dy, dz, true, false);
+    return __ldg(at(a, dx, dy, dz));
+  }
+  __device__ __forceinline__ void write(int a, double v) const {
+    TCG_CHECK_ACCESS(a, 0, 0, 0, false, true);
+    *c[a] = v;
+  }
+  __device__ __forceinline__ void increment(int a, double v) const {
+    TCG_CHECK_ACCESS(a, 0, 0, 0, true, true);
+    *c[a] = __ldg(c[a]) + v;
+  }
   __device__ __forceinline__ void contribute(double v) {
     if (L.masked && (px < L.mlo[0] || px >= L.mhi[0] || py < L.mlo[1] || py >= L.mhi[1] || pz < L.mlo[2] ||
                      pz >= L.mhi[2]))
@@ -943,6 +988,12 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
     for (int a = 0; a < lp.nargs; ++a) {
       const DevView v = view(ch.dat_ids.empty() ? lp.args[a].dat : ch.dat_ids[static_cast<size_t>(lp.args[a].dat)], false);
       L.a[a] = UArg{v.base, v.x0, v.y0, v.z0, v.py, v.pz, lp.args[a].mode, lp.args[a].stencil};
+#ifdef TCG_CHECKED
+      for (int d = 0; d < 3; ++d) {
+        L.alo[a][d] = v.alo[d];
+        L.ahi[a][d] = v.ahi[d];
+      }
+#endif
     }
     L.st = cd.st;
     L.pf = prefetch ? 1 : 0;
