@@ -517,6 +517,7 @@ DeviceExec::DeviceExec() {
   TCG_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   stream_ = st;
   TCG_CK(cudaMalloc(&red_dev_, sizeof(double) * 64));
+  TCG_CK(cudaMallocHost(&red_host_, sizeof(double) * 64));
 }
 
 DeviceExec::~DeviceExec() {
@@ -537,6 +538,7 @@ DeviceExec::~DeviceExec() {
   if (scratch_) cudaFree(scratch_);
   if (partials_) cudaFree(partials_);
   if (red_dev_) cudaFree(red_dev_);
+  if (red_host_) cudaFreeHost(red_host_);
   if (staging_) cudaFree(staging_);
   if (redbuf_) cudaFree(redbuf_);
   drop_graphs();
@@ -778,6 +780,15 @@ void DeviceExec::upload_async(int f, const double* host) {
 void DeviceExec::download_async(int f, double* host) {
   Buf* b = fields_.at(static_cast<size_t>(f));
   copy2d(*this, f, b->mem[b->cur], b->x0, b->py, b->alloc, host, false, true, static_cast<cudaStream_t>(stream_));
+}
+
+// Chain reductions to the host through a pinned buffer (a pageable
+// destination would take the driver's staged copy path on every flush).
+void DeviceExec::read_reductions(double* out, int n) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  TCG_CK(cudaMemcpyAsync(red_host_, red_dev_, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, st));
+  TCG_CK(cudaStreamSynchronize(st));
+  std::memcpy(out, red_host_, sizeof(double) * static_cast<size_t>(n));
 }
 
 void DeviceExec::synchronize() { TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_))); }
@@ -1208,8 +1219,7 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
     }
   }
   if (ch.nred > 0) {
-    TCG_CK(cudaMemcpyAsync(red_out, red_dev_, sizeof(double) * static_cast<size_t>(ch.nred), cudaMemcpyDeviceToHost, st));
-    TCG_CK(cudaStreamSynchronize(st));
+    read_reductions(red_out, ch.nred);
   }
 }
 

@@ -400,9 +400,7 @@ void DeviceExec::run_l2(const DevChain& ch, const std::vector<DevItem>& items, c
     ++launches_;
   }
   if (ch.nred > 0) {
-    TCG_CK(cudaMemcpyAsync(red_out, red_dev_, sizeof(double) * static_cast<size_t>(ch.nred), cudaMemcpyDeviceToHost,
-                           st));
-    TCG_CK(cudaStreamSynchronize(st));
+    read_reductions(red_out, ch.nred);
   }
 }
 

@@ -134,8 +134,7 @@ void DeviceExec::run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t 
     ++launches_;
   }
   if (gp.nred > 0) {
-    TCG_CK(cudaMemcpyAsync(red_out, red_dev_, sizeof(double) * static_cast<size_t>(gp.nred), cudaMemcpyDeviceToHost, st));
-    TCG_CK(cudaStreamSynchronize(st));
+    read_reductions(red_out, gp.nred);
   }
 }
 

@@ -102,6 +102,8 @@ class DeviceExec {
               const std::array<int32_t, 3>& reach, uint64_t plan_key, double* red_out);
 
   void synchronize();
+  // Copies the first n chain-reduction slots to `out` (syncs the stream).
+  void read_reductions(double* out, int n);
   void* stream() const { return stream_; }
   int64_t launches() const { return launches_; }
   // Kernel timing: when enabled, CUDA events bracket every main executor
@@ -130,6 +132,7 @@ class DeviceExec {
   double* partials_ = nullptr;
   size_t partials_n_ = 0;
   double* red_dev_ = nullptr;
+  double* red_host_ = nullptr;  // pinned
   double* staging_ = nullptr;
   size_t staging_n_ = 0;
   double* redbuf_ = nullptr;
