@@ -663,6 +663,19 @@ void DeviceExec::buf_to_field(int f, const Range& box, const double* buf, const 
   copy_box(fb, dense_buf(const_cast<double*>(buf), buf_box), box, static_cast<cudaStream_t>(stream_));
 }
 
+void DeviceExec::fill_box_bytes(int f, const Range& box, int byte) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  if (!b->alloc.contains(box)) throw AccessError("fill_box_bytes: " + box.to_string() + " outside " + b->alloc.to_string());
+  if (box.empty()) return;
+  double* base = b->mem[b->cur] + ((lo_of(box, 2) - lo_of(b->alloc, 2)) * b->pz + (lo_of(box, 1) - lo_of(b->alloc, 1)) * b->py +
+                                   (lo_of(box, 0) - b->x0));
+  const cudaPitchedPtr pp = make_cudaPitchedPtr(base, static_cast<size_t>(b->py) * 8, static_cast<size_t>(b->py) * 8,
+                                                static_cast<size_t>(b->ny));
+  const cudaExtent ext = make_cudaExtent(static_cast<size_t>(ext_of(box, 0)) * 8, static_cast<size_t>(ext_of(box, 1)),
+                                         static_cast<size_t>(ext_of(box, 2)));
+  TCG_CK(cudaMemset3DAsync(pp, byte, ext, static_cast<cudaStream_t>(stream_)));
+}
+
 void DeviceExec::copy_within(int f, const Range& box, const Point& shift) {
   Buf* b = fields_.at(static_cast<size_t>(f));
   Range src(box.dim());

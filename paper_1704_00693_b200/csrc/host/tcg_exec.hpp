@@ -73,6 +73,9 @@ class DeviceExec {
   void buf_to_field(int f, const Range& box, const double* buf, const Range& buf_box);
   // Copy box + shift -> box inside field f (periodic ghost layers).
   void copy_within(int f, const Range& dst_box, const Point& shift);
+  // Sets every byte of box (inside field f's allocation) to `byte`
+  // (0xFF: every double a NaN -- the halo-poisoning tripwire).
+  void fill_box_bytes(int f, const Range& box, int byte);
   // Periodic ghost fill of fields (all with the same logical box), all
   // dimensions in order (edges/corners wrap), one kernel launch per dimension.
   void periodic_fill(const std::vector<int>& fields, const Range& logical, int64_t depth);

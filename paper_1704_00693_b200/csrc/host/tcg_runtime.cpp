@@ -102,6 +102,7 @@ std::string ExecutionReport::to_text() const {
 }
 
 Runtime::Runtime(int dim, RuntimeConfig cfg) : dim_(dim), cfg_(cfg) {
+  if (const char* e = std::getenv("TCG_POISON_HALOS")) poison_ = std::atoi(e) != 0;
   if (dim < 1 || dim > kMaxDims) throw InvalidArgument("Runtime: block dim must be 1, 2, or 3");
   if (cfg_.threads < 1) throw InvalidArgument("Runtime: threads must be >= 1");
   if (cfg_.skew_allowance < 0) throw InvalidArgument("Runtime: skew_allowance must be >= 0");
@@ -1051,6 +1052,42 @@ DistSchedule Runtime::schedule_pending() {
   return s;
 }
 
+// DistContext::poison_stale_halos (dist.cpp:546-586): on every local rank,
+// the points of each interior face strip (allocation beyond the owned box
+// towards a neighbour) that this chain or an earlier one writes become NaN
+// before the chain runs; their correct values can arrive only through the
+// exchange or a local recompute, so a gap in the schedule shows up as NaN.
+void Runtime::poison_stale_halos(const LoopChain& chain) {
+  std::map<DatasetId, std::vector<Range>> writes;
+  for (const LoopRecord& lp : chain.loops)
+    for (const ArgSpec& a : lp.args)
+      if (mode_writes(a.mode)) writes[a.dataset].push_back(lp.range);
+  for (const auto& [ds, boxes] : dist_->written)
+    for (const Range& b : boxes) writes[ds].push_back(b);
+  DeviceExec& dev = device();
+  const RankLayout& lay = dist_->layout;
+  for (int r : dist_->local) {
+    const Range& own = lay.owned[static_cast<size_t>(r)];
+    const Target& t = dist_->targets[static_cast<size_t>(r)];
+    for (const auto& [ds, boxes] : writes) {
+      const Range& alloc = t.alloc[static_cast<size_t>(ds)];
+      for (int d = 0; d < lay.dim; ++d)
+        for (int dir : {-1, +1}) {
+          if (lay.neighbor(r, d, dir) < 0) continue;
+          Range strip = alloc;
+          if (dir < 0)
+            strip.set(d, alloc.start(d), own.start(d));
+          else
+            strip.set(d, own.end(d), alloc.end(d));
+          for (const Range& w : boxes) {
+            const Range x = strip.intersect(w);
+            if (!x.empty()) dev.fill_box_bytes(t.dev[static_cast<size_t>(ds)], x, 0xFF);
+          }
+        }
+    }
+  }
+}
+
 void Runtime::exchange(const DistSchedule& s, ExecutionReport& rep) {
   DeviceExec& dev = device();
   std::vector<char> is_local(static_cast<size_t>(dist_->layout.rank_count()), 0);
@@ -1122,6 +1159,7 @@ ExecutionReport Runtime::execute_distributed(LoopChain chain, const ExecMode& mo
   DeviceExec& dev = device();
   const int64_t l0 = dev.launches();
   const bool on_demand = mode.kind == ExecMode::Kind::Untiled;
+  if (poison_) poison_stale_halos(chain);
   // Stages: (schedule, loops [begin, end) of the chain it covers).
   std::vector<std::shared_ptr<const DistSchedule>> stages;
   if (on_demand) {

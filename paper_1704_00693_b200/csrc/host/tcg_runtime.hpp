@@ -186,6 +186,8 @@ class Runtime {
   void drop_dist();
   std::shared_ptr<const DistSchedule> dist_schedule(const LoopChain& chain);
   void exchange(const DistSchedule& s, ExecutionReport& rep);
+  void poison_stale_halos(const LoopChain& chain);
+  bool poison_ = false;  // TCG_POISON_HALOS=1 (debug tripwire, dist.cpp:546-586)
   int root_for(DatasetId ds, const Point& p);
   DevChain lower(const LoopChain& chain, const Target& t) const;
   void run_tiled(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep, const Target& t,
