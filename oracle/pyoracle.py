@@ -83,6 +83,7 @@ def load_ref():
             "tcref_fetch": [_P, ctypes.c_int, _P],
             "tcref_last_plan": [_P, ctypes.c_char_p, _I64],
             "tcref_plan_pending": [_P, _P, ctypes.c_char_p, _I64],
+            "tcref_validate_plan": [_P, _P, _P, _I64, ctypes.c_int, ctypes.c_char_p, _I64],
             "tcref_rank_plans_pending": [_P, _P, _P, ctypes.c_char_p, _I64],
             "tcref_dist_info": [_P, ctypes.c_char_p, _I64],
             "tcref_auto_tile_size": [ctypes.c_int, _I64, ctypes.c_int, _I64, _P, _P],
@@ -277,6 +278,19 @@ class RefRuntime(_Base):
     def plan_pending(self, ts):
         ts = list(ts) + [0] * (3 - len(ts))
         return self._text(self.lib.tcref_plan_pending, _arr(_I64, ts[:3]))
+
+    def validate_plan_pending(self, ts, ranges, ntiles, nloops):
+        """The reference's validate_dependencies + validate_coverage
+        (oracle.cpp:154-284) on an external plan for the pending chain
+        (consumed). ranges: flat int64, 6 per (tile, loop). Returns
+        (violation count, text)."""
+        ts = list(ts) + [0] * (3 - len(ts))
+        buf = ctypes.create_string_buffer(1 << 20)
+        n = self.lib.tcref_validate_plan(self.h, _arr(_I64, ts[:3]), _arr(_I64, ranges), ntiles, nloops, buf,
+                                         len(buf))
+        if n < 0:
+            raise OracleError(self.lib.tcref_error().decode())
+        return int(n), buf.value.decode()
 
     def rank_plans_pending(self, grid, ts):
         g = list(grid) + [1] * (3 - len(grid))

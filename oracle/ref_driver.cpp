@@ -284,6 +284,37 @@ int64_t tcref_plan_pending(void* hv, const int64_t* ts3, char* buf, int64_t n) {
   });
 }
 
+// Consumes the pending queue: the reference's own validators
+// (validate_dependencies / validate_coverage, oracle.cpp:154-284) applied to
+// an externally built plan for that chain -- ranges[(t*L + l)*6 + 2d + {0,1}]
+// over the tile grid of compute_union_bounds(chain, ts). Returns the number of
+// violations; their text goes to buf.
+int64_t tcref_validate_plan(void* hv, const int64_t* ts3, const int64_t* ranges, int64_t ntiles, int32_t nloops,
+                            char* buf, int64_t n) {
+  auto* h = static_cast<Handle*>(hv);
+  int64_t count = -1;
+  const int64_t rc = guarded([&]() -> int64_t {
+    LoopChain chain = h->rt->take_pending();
+    PlanConfig cfg = compute_union_bounds(chain, {ts3[0], ts3[1], ts3[2]});
+    if (cfg.total_tiles() != ntiles || static_cast<int32_t>(chain.size()) != nloops)
+      throw InvalidArgument("validate_plan: plan shape does not match the chain's tile grid");
+    std::vector<Range> rs;
+    for (int64_t i = 0; i < ntiles * nloops; ++i) {
+      Range r(chain.dim);
+      for (int d = 0; d < chain.dim; ++d) r.set(d, ranges[i * 6 + 2 * d], ranges[i * 6 + 2 * d + 1]);
+      rs.push_back(r);
+    }
+    TilingPlan plan(cfg, chain.signature(), nloops, std::move(rs), {}, 0.0);
+    std::vector<oracle::Violation> v = oracle::validate_dependencies(plan, chain, 32);
+    for (const oracle::Violation& x : oracle::validate_coverage(plan, chain, 32)) v.push_back(x);
+    std::ostringstream os;
+    for (const oracle::Violation& x : v) os << x.to_string() << "\n";
+    count = static_cast<int64_t>(v.size());
+    return put_text(os.str(), buf, n);
+  });
+  return rc < 0 ? rc : count;
+}
+
 // Consumes the pending queue; per rank of decompose(global, grid):
 // construct_rank_plan (dist.cpp:191-390) + compute_halo_depths (:407-448).
 int64_t tcref_rank_plans_pending(void* hv, const int* g3, const int64_t* ts3, char* buf, int64_t n) {

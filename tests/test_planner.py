@@ -221,3 +221,60 @@ def test_par_loop_validation():
         rt.fetch_reduction(-1)
     with pytest.raises(InvalidArgument):
         rt.fetch_reduction(42)
+
+
+def _plan_ranges(text, dim):
+    """TilingPlan::dump text (planner.cpp:234-250) -> flat ranges, T, L."""
+    rows = {}
+    for line in text.splitlines():
+        if not line.startswith("tile="):
+            continue
+        f = line.split()
+        t, l, d = int(f[0][5:]), int(f[1][5:]), int(f[2][2:])
+        s, e = f[3].strip("[)").split(",")
+        rows[(t, l, d)] = (int(s), int(e))
+    T = 1 + max(k[0] for k in rows)
+    L = 1 + max(k[1] for k in rows)
+    flat = []
+    for t in range(T):
+        for l in range(L):
+            for d in range(3):
+                flat += list(rows[(t, l, d)]) if d < dim else [0, 1]
+    return flat, T, L
+
+
+def test_reference_validators_accept_our_plans(ref_lib):
+    # §8(f) row 3: the reference's own validate_dependencies and
+    # validate_coverage (oracle.cpp:154-284) run on the plans this
+    # repository's planner builds; a plan with one loop range shrunk is
+    # rejected (the validators are live).
+    checked = 0
+    for dim, seeds, kw in ((2, range(600, 630), {}), (1, range(700, 710), {"extent": (32, 96)}),
+                           (3, range(800, 806), {"extent": (8, 16)})):
+        for seed in seeds:
+            gc = C.generate(seed, dim=dim, **kw)
+            ts = C.random_tile_sizes(seed, dim)
+            rt = Runtime(dim)
+            rt.upload = lambda ds, a: None
+            C.declare(rt, gc)
+            C.enqueue(rt, gc)
+            flat, T, L = _plan_ranges(rt.plan_pending(ts), dim)
+            ref = ref_lib.RefRuntime(dim)
+            C.declare(ref, gc)
+            C.enqueue(ref, gc)
+            n, text = ref.validate_plan_pending(ts, flat, T, L)
+            assert n == 0, (dim, seed, text)
+            checked += 1
+            if seed == seeds[0]:
+                # Shrink the first non-empty range by one point: coverage gap.
+                bad = list(flat)
+                for i in range(0, len(bad), 6):
+                    if all(bad[i + 2 * d] < bad[i + 2 * d + 1] for d in range(dim)):
+                        bad[i + 1] -= 1
+                        break
+                ref2 = ref_lib.RefRuntime(dim)
+                C.declare(ref2, gc)
+                C.enqueue(ref2, gc)
+                n2, _ = ref2.validate_plan_pending(ts, bad, T, L)
+                assert n2 > 0, (dim, seed)
+    assert checked == 46
