@@ -94,7 +94,7 @@ def _run_config(rt, cfg_cls, n, **kw):
     raise ValueError(cfg_cls)
 
 
-@pytest.mark.parametrize("cfg,n", [(configs.HeatC1, 64), (configs.HydroC2, 96), (configs.Jacobi3DC3, 24)])
+@pytest.mark.parametrize("cfg,n", [(configs.HeatC1, 64), (configs.HydroC2, 96), (configs.HydroC2, 90), (configs.Jacobi3DC3, 24)])
 @pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled((0, 0, 0)), ExecMode.windowed(),
                                   ExecMode.tiled_auto()])
 def test_configs_small_match_oracle(oracle_lib, cfg, n, mode):
