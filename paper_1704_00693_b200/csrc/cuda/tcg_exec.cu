@@ -199,7 +199,7 @@ struct BatchReads {
   static constexpr int kReads = BODY == tcb::kHydroCfl ? 3 : 0;
 };
 
-constexpr int kBatchRows = 4;
+constexpr int kBatchRows = 2;
 
 template <int N>
 struct PreAcc {
@@ -277,8 +277,8 @@ __device__ __forceinline__ void untiled_block(const ULaunch& L) {
       constexpr int kNR = BatchReads<BODY>::kReads;
       if (kNR > 0 && nr == kUntiledRun) {
         // Chunks of kBatchRows rows: 2D runs sit under a 6-blocks/SM
-        // register budget, and a whole 8-row run buffered (24 doubles)
-        // spills (measured 92 -> 100 us on c2's CFL loop).
+        // register budget. Measured on c2's CFL loop (plain 91.7 us):
+        // 2-row chunks 76.3, 4-row 82.6, the whole 8-row run 100 (spills).
         constexpr int kChunk = kUntiledRun < kBatchRows ? kUntiledRun : kBatchRows;
 #pragma unroll
         for (int c0 = 0; c0 < kUntiledRun; c0 += kChunk) {
