@@ -204,6 +204,8 @@ def parse_mode(s):
         return ExecMode.tiled([int(v) for v in s[6:].split(",")])
     if s == "windowed":
         return ExecMode.windowed()
+    if s == "stream":
+        return ExecMode.stream()
     if s.startswith("windowed:"):
         return ExecMode.windowed([int(v) for v in s[9:].split(",")])
     raise ValueError(s)
@@ -416,7 +418,7 @@ def main():
     del rt, cfg, step
     fixed = {}
     if not args.no_untiled:
-        for mname in ("untiled", "tiled:0,0,0", "windowed"):
+        for mname in ("untiled", "stream"):
             if mname == args.mode:
                 continue
             rtu, cfgu, stepu = build(parse_mode(mname))
@@ -426,8 +428,8 @@ def main():
             fixed[mname] = cu * args.steps / (max_over_ranks(msu, dist) / 1e3)
             del rtu, cfgu, stepu
     untiled_value = fixed.get("untiled", value if args.mode == "untiled" else None)
-    tiled_value = fixed.get("tiled:0,0,0")
-    windowed_value = fixed.get("windowed")
+    tiled_value = fixed.get("stream", value if args.mode == "stream" else None)
+    windowed_value = None
 
     # ---- end-to-end through the public API with host buffers --------------------
     e2e = None

@@ -66,8 +66,10 @@ enum { TCG_RED_NONE = -1, TCG_RED_SUM = 0, TCG_RED_MIN = 1, TCG_RED_MAX = 2 };
  * plan (tile_sizes as in the reference, 0 = GPU sizer) on the L2-resident
  * executor; TCG_WINDOWED selects the shared-memory windowed executor
  * (tile_sizes = column block / stream tile bounds, 0 = sizer); TCG_TILED_AUTO
- * times the executors per chain and keeps the fastest. */
-enum { TCG_UNTILED = 0, TCG_TILED = 1, TCG_TILED_AUTO = 2, TCG_WINDOWED = 3 };
+ * times the executors per chain and keeps the fastest. TCG_STREAM runs the
+ * fused streaming executor: one kernel per chain signature, generated and
+ * compiled for sm_100a at run time. */
+enum { TCG_UNTILED = 0, TCG_TILED = 1, TCG_TILED_AUTO = 2, TCG_WINDOWED = 3, TCG_STREAM = 4 };
 
 typedef struct tcg_runtime tcg_runtime;
 
@@ -131,6 +133,15 @@ int tcg_rank_plans_pending(tcg_runtime* rt, const int32_t grid[3], const int64_t
 int tcg_gpu_plan_pending(tcg_runtime* rt, int mode, const int64_t tile_sizes[3], char* buf, int64_t n,
                          int64_t* needed);
 int tcg_signature_pending(tcg_runtime* rt, uint64_t* out);
+/* Streaming executor (the B200 form of execute_plan over the skewed tile
+ * plan, executor.cpp:209-250 / planner.cpp:55-208). cfg: {threads per CTA,
+ * points per thread x, points per thread y, threads along x, stream segments,
+ * loops per kernel, min CTAs per SM, L2 prefetch rows}; 0 (prefetch -1) =
+ * sizer. tcg_stream_plan_pending consumes the pending chain and returns the
+ * plan summary; what & 1: also compile every kernel with NVRTC (no GPU
+ * needed) and append the compiler log; what & 2: append the sources. */
+int tcg_set_stream_choice(tcg_runtime* rt, const int32_t cfg[8]);
+int tcg_stream_plan_pending(tcg_runtime* rt, int what, char* buf, int64_t n, int64_t* needed);
 
 /* Distribution. grid: ranks per dimension (slabs: {1,P,1}
  * in 2D, {1,1,P} in 3D). tcg_set_rank_grid hosts every rank in this process

@@ -27,15 +27,16 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra", "-Wno-unused-parameter",
-            f"-I{REPO / 'include'}", "-I/usr/local/cuda/include"]
+            f"-I{REPO / 'include'}", "-I/usr/local/cuda/include", f"-I{OBJ_DIR}"]
 NVCCFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler", "-fPIC",
                     "--expt-relaxed-constexpr", "-Xptxas", "-v", f"-I{REPO / 'include'}"]
 
 if DEBUG:
     NVCCFLAGS = NVCCFLAGS + ["-DTCG_DEBUG_PRINT"]
 
-HOST_SRCS = ["host/tcg_plan.cpp", "host/tcg_gpuplan.cpp", "host/tcg_dist.cpp", "host/tcg_runtime.cpp", "tcg_capi.cpp"]
-CUDA_SRCS = ["cuda/tcg_exec.cu", "cuda/tcg_tiled.cu", "cuda/tcg_l2.cu", "cuda/tcg_comm.cu"]
+HOST_SRCS = ["host/tcg_plan.cpp", "host/tcg_gpuplan.cpp", "host/tcg_dist.cpp", "host/tcg_stream.cpp", "host/tcg_jit.cpp",
+             "host/tcg_runtime.cpp", "tcg_capi.cpp"]
+CUDA_SRCS = ["cuda/tcg_exec.cu", "cuda/tcg_tiled.cu", "cuda/tcg_l2.cu", "cuda/tcg_comm.cu", "cuda/tcg_stream_exec.cu"]
 
 
 def _headers() -> list[Path]:
@@ -60,8 +61,23 @@ def _compile(cmd: list[str], log: Path) -> None:
         raise RuntimeError(f"compile failed: {' '.join(cmd)}")
 
 
+def _embed_bodies() -> None:
+    """Writes tcb_sources.inc: the body registry headers as string literals,
+    handed to NVRTC when a generated chain kernel is compiled (tcg_jit.cpp)."""
+    out = OBJ_DIR / "tcb_sources.inc"
+    parts = []
+    for var, name in (("kTcbBodiesSrc", "tc_bodies.h"), ("kTcbNsSrc", "tc_ns.h")):
+        text = (CSRC / "kernels" / name).read_text()
+        assert ")TCBSRC\"" not in text
+        parts.append(f'const char* const {var} = R"TCBSRC({text})TCBSRC";\n')
+    data = "".join(parts)
+    if not out.exists() or out.read_text() != data:
+        out.write_text(data)
+
+
 def build(verbose: bool = False) -> Path:
     OBJ_DIR.mkdir(parents=True, exist_ok=True)
+    _embed_bodies()
     headers = _headers()
     jobs = []
     objs = []
@@ -92,11 +108,11 @@ def build(verbose: bool = False) -> Path:
             for f in [ex.submit(_compile, c, l) for c, l in allj]:
                 f.result()
     if jobs or not LIB.exists():
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcuda", "-ldl"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lnvrtc", "-ldl", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
         _compile(cmd, LIB_DIR / "link.log")
     if jobs or checked_jobs or not LIB_CHECKED.exists():
         cobjs = [str(cobj) if o.name == "cuda_tcg_exec.cu.o" else str(o) for o in objs]
-        _compile([NVCC, *ARCH, "-shared", "-o", str(LIB_CHECKED), *cobjs, "-lcuda", "-ldl"], LIB_DIR / "link_checked.log")
+        _compile([NVCC, *ARCH, "-shared", "-o", str(LIB_CHECKED), *cobjs, "-lnvrtc", "-ldl", "-Xlinker", "-rpath=/usr/local/cuda/lib64"], LIB_DIR / "link_checked.log")
     if verbose:
         print(f"built {LIB}")
     return LIB

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "../host/tcg_exec.hpp"
 #include "../kernels/tc_bodies.h"
@@ -144,6 +145,10 @@ struct DeviceExec::Buf {
   double* mem[2] = {nullptr, nullptr};
   size_t bytes = 0;
   int cur = 0;
+  // Streaming executor bookkeeping: boxes where the second buffer may differ
+  // from the current one (alt_synced false: anywhere).
+  std::vector<Range> dirty;
+  bool alt_synced = false;
 };
 
 struct DeviceExec::PlanBufs {

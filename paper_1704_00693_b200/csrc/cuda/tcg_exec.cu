@@ -626,6 +626,10 @@ DeviceExec::~DeviceExec() {
   if (red_host_) cudaFreeHost(red_host_);
   if (staging_) cudaFree(staging_);
   if (redbuf_) cudaFree(redbuf_);
+  if (st_part_) cudaFree(st_part_);
+  if (st_out_) cudaFree(st_out_);
+  if (st_ticket_) cudaFree(st_ticket_);
+  if (host_stage_) cudaFreeHost(host_stage_);
   drop_graphs();
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
 }
@@ -634,14 +638,17 @@ int DeviceExec::add_field(const Range& alloc) {
   auto* b = new Buf;
   b->alloc = alloc;
   const int dim = alloc.dim();
-  const int64_t ax0 = alloc.start(0), ax1 = alloc.end(0);
-  // x origin: a multiple of 16 at least 16 elements before the allocation.
-  auto fl16 = [](int64_t v) { return v >= 0 ? v / 16 * 16 : -((-v + 15) / 16) * 16; };
-  b->x0 = fl16(ax0) - 16;
-  b->py = ((ax1 + 16 - b->x0) + 15) / 16 * 16;
-  b->ny = dim >= 2 ? alloc.extent(1) : 1;
-  b->nz = dim >= 3 ? alloc.extent(2) : 1;
-  b->pz = b->py * b->ny;
+  int64_t lo[3], hi[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = d < dim ? alloc.start(d) : 0;
+    hi[d] = d < dim ? alloc.end(d) : 1;
+  }
+  const FieldLayout fl = field_layout(dim, lo, hi);
+  b->x0 = fl.x0;
+  b->py = fl.py;
+  b->ny = fl.ny;
+  b->nz = fl.nz;
+  b->pz = fl.pz;
   b->bytes = static_cast<size_t>(b->pz * b->nz) * sizeof(double);
   TCG_CK(cudaMalloc(&b->mem[0], b->bytes));
   TCG_CK(cudaMemsetAsync(b->mem[0], 0, b->bytes, static_cast<cudaStream_t>(stream_)));
@@ -686,15 +693,23 @@ double* point_addr(const DevView& v, const Range& alloc, const Point& p) {
 double DeviceExec::get_point(int f, const Point& p) {
   const DevView v = view(f, false);
   double out = 0;
-  TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
-  TCG_CK(cudaMemcpy(&out, point_addr(v, fields_.at(static_cast<size_t>(f))->alloc, p), 8, cudaMemcpyDeviceToHost));
+  read_device(&out, point_addr(v, fields_.at(static_cast<size_t>(f))->alloc, p), 1);
   return out;
 }
 
 void DeviceExec::put_point(int f, const Point& p, double val) {
   const DevView v = view(f, false);
-  TCG_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
-  TCG_CK(cudaMemcpy(point_addr(v, fields_.at(static_cast<size_t>(f))->alloc, p), &val, 8, cudaMemcpyHostToDevice));
+  double* dst = point_addr(v, fields_.at(static_cast<size_t>(f))->alloc, p);
+  // Stream-ordered through the pinned staging buffer (a pageable source may
+  // return before the copy lands, and the executor stream is non-blocking).
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  TCG_CK(cudaStreamSynchronize(st));
+  red_host_[0] = val;
+  TCG_CK(cudaMemcpyAsync(dst, red_host_, 8, cudaMemcpyHostToDevice, st));
+  TCG_CK(cudaStreamSynchronize(st));
+  Range box(fields_.at(static_cast<size_t>(f))->alloc.dim());
+  for (int d = 0; d < box.dim(); ++d) box.set(d, p[d], p[d] + 1);
+  mark_written(f, box);
 }
 
 namespace {
@@ -746,6 +761,7 @@ void DeviceExec::buf_to_field(int f, const Range& box, const double* buf, const 
                       buf_box.to_string());
   const BoxBuf fb{b->mem[b->cur], b->x0, lo_of(b->alloc, 1), lo_of(b->alloc, 2), b->py, b->ny};
   copy_box(fb, dense_buf(const_cast<double*>(buf), buf_box), box, static_cast<cudaStream_t>(stream_));
+  mark_written(f, box);
 }
 
 void DeviceExec::fill_box_bytes(int f, const Range& box, int byte) {
@@ -759,6 +775,7 @@ void DeviceExec::fill_box_bytes(int f, const Range& box, int byte) {
   const cudaExtent ext = make_cudaExtent(static_cast<size_t>(ext_of(box, 0)) * 8, static_cast<size_t>(ext_of(box, 1)),
                                          static_cast<size_t>(ext_of(box, 2)));
   TCG_CK(cudaMemset3DAsync(pp, byte, ext, static_cast<cudaStream_t>(stream_)));
+  mark_written(f, box);
 }
 
 void DeviceExec::copy_within(int f, const Range& box, const Point& shift) {
@@ -780,6 +797,7 @@ void DeviceExec::copy_within(int f, const Range& box, const Point& shift) {
                              static_cast<size_t>(ext_of(box, 2)));
   p.kind = cudaMemcpyDeviceToDevice;
   TCG_CK(cudaMemcpy3DAsync(&p, static_cast<cudaStream_t>(stream_)));
+  mark_written(f, box);
 }
 
 void DeviceExec::periodic_fill(const std::vector<int>& fields, const Range& logical, int64_t depth) {
@@ -812,6 +830,23 @@ void DeviceExec::periodic_fill(const std::vector<int>& fields, const Range& logi
       TCG_CK(cudaGetLastError());
       ++launches_;
     }
+  }
+  // Ghost layers written: the slabs outside the logical box, every dimension.
+  for (int f : fields) {
+    const Range& al = fields_.at(static_cast<size_t>(f))->alloc;
+    for (int d = 0; d < dim; ++d)
+      for (int side = 0; side < 2; ++side) {
+        Range g(dim);
+        for (int e = 0; e < dim; ++e) {
+          const int64_t w = e < d ? depth : 0;
+          g.set_raw(e, logical.start(e) - w, logical.end(e) + w);
+        }
+        if (side == 0)
+          g.set_raw(d, logical.start(d) - depth, logical.start(d));
+        else
+          g.set_raw(d, logical.end(d), logical.end(d) + depth);
+        mark_written(f, g.intersect(al));
+      }
   }
 }
 
@@ -863,6 +898,7 @@ void copy2d(DeviceExec& ex, int f, double* dev, int64_t x0, int64_t py, const Ra
 
 void DeviceExec::upload(int f, const double* host) {
   Buf* b = fields_.at(static_cast<size_t>(f));
+  mark_written(f, b->alloc);
   copy2d(*this, f, b->mem[b->cur], b->x0, b->alloc.dim() >= 2 ? b->py : b->py, b->alloc, const_cast<double*>(host),
          true, false, static_cast<cudaStream_t>(stream_));
 }
@@ -872,6 +908,7 @@ void DeviceExec::download(int f, double* host) {
 }
 void DeviceExec::upload_async(int f, const double* host) {
   Buf* b = fields_.at(static_cast<size_t>(f));
+  mark_written(f, b->alloc);
   copy2d(*this, f, b->mem[b->cur], b->x0, b->py, b->alloc, const_cast<double*>(host), true, true,
          static_cast<cudaStream_t>(stream_));
 }
@@ -1021,6 +1058,7 @@ void DeviceExec::drop_graphs() {
 }
 
 void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
+  mark_chain_writes(ch);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   void* scratch = ensure_scratch(chain_bytes(ch));
   const ChainDev cd = upload_chain(ch, scratch, st, &scratch_hash_);

@@ -296,6 +296,7 @@ int l2_grid(const DeviceInfo& info) {
 
 void DeviceExec::run_l2(const DevChain& ch, const std::vector<DevItem>& items, const std::vector<int32_t>& deps,
                         const std::array<int32_t, 3>& reach, uint64_t key, double* red_out) {
+  mark_chain_writes(ch);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   if (ch.dat_ids.size() > static_cast<size_t>(kMaxChainDats))
     throw PlanError("tiled executor: chain touches more than 32 datasets");

@@ -72,6 +72,7 @@ DeviceExec::PlanBufs* DeviceExec::plan_bufs(const GpuTiledPlan& gp, uint64_t key
 }
 
 void DeviceExec::run_tiled(const DevChain& ch, const GpuTiledPlan& gp, uint64_t key, double* red_out) {
+  mark_chain_writes(ch);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   PlanBufs* pb = plan_bufs(gp, key);
   void* scratch = ensure_scratch(chain_bytes(ch));

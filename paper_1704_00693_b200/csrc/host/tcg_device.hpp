@@ -19,6 +19,23 @@ constexpr int kL2Run = 4;  // 8 measured: c1 -7%, c3 -9%, c2 +18% (tools/ab_l2ru
 // (so even x is 16-byte aligned, x % 16 == 0 is 128-byte aligned) and py is a
 // multiple of 16 elements. The buffer has >= 16 elements of slack before the
 // allocation's first point and after its last point in x.
+// Layout of a field buffer over allocation box [lo, hi) (dim 0 fastest):
+// x origin a multiple of 16 at least 16 elements before the allocation, row
+// pitch a multiple of 16 elements.
+struct FieldLayout {
+  int64_t x0, py, ny, nz, pz;
+};
+inline FieldLayout field_layout(int dim, const int64_t lo[3], const int64_t hi[3]) {
+  auto fl16 = [](int64_t v) { return v >= 0 ? v / 16 * 16 : -((-v + 15) / 16) * 16; };
+  FieldLayout L;
+  L.x0 = fl16(lo[0]) - 16;
+  L.py = ((hi[0] + 16 - L.x0) + 15) / 16 * 16;
+  L.ny = dim >= 2 ? hi[1] - lo[1] : 1;
+  L.nz = dim >= 3 ? hi[2] - lo[2] : 1;
+  L.pz = L.py * L.ny;
+  return L;
+}
+
 struct DevView {
   double* base;
   int64_t x0, y0, z0;

@@ -104,6 +104,24 @@ class DeviceExec {
   void run_l2(const DevChain& ch, const std::vector<DevItem>& items, const std::vector<int32_t>& deps,
               const std::array<int32_t, 3>& reach, uint64_t plan_key, double* red_out);
 
+  // ---- streaming executor support (csrc/cuda/tcg_stream_exec.cu) ----
+  // Box of field f's current buffer written by anything but a streaming
+  // kernel: the second buffer may differ there from now on.
+  void mark_written(int f, const Range& box);
+  // Makes field f's second buffer equal to its current one outside `keep`
+  // (allocating and copying it whole on first use).
+  void sync_alt(int f, const Range& keep);
+  // A streaming kernel stored `box` into f's second buffer: swap the buffers;
+  // the new second buffer differs from the new current one inside `box`.
+  void commit_alt(int f, const Range& box);
+  // mark_written for every write of a lowered chain (untiled / L2 / windowed).
+  void mark_chain_writes(const DevChain& ch);
+  // Reduction scratch of a streaming launch: CTA partials, results, ticket.
+  void stream_red_buffers(size_t npart, size_t nout, double** part, double** out, unsigned** ticket);
+  void launch_stream(void* fn, int64_t grid, int nt, int smem, const void* args, size_t bytes);
+  // Device -> host through the pinned staging buffer (syncs the stream).
+  void read_device(double* host, const double* dev, size_t n);
+
   void synchronize();
   // Copies the first n chain-reduction slots to `out` (syncs the stream).
   void read_reductions(double* out, int n);
@@ -135,6 +153,13 @@ class DeviceExec {
   double* partials_ = nullptr;
   size_t partials_n_ = 0;
   double* red_dev_ = nullptr;
+  double* st_part_ = nullptr;
+  size_t st_part_n_ = 0;
+  double* st_out_ = nullptr;
+  size_t st_out_n_ = 0;
+  unsigned* st_ticket_ = nullptr;
+  double* host_stage_ = nullptr;  // pinned
+  size_t host_stage_n_ = 0;
   double* red_host_ = nullptr;  // pinned
   double* staging_ = nullptr;
   size_t staging_n_ = 0;

@@ -6,6 +6,7 @@
 #include <limits>
 
 #include "../kernels/tc_bodies.h"
+#include "tcg_jit.hpp"
 
 namespace tcg {
 
@@ -106,17 +107,23 @@ Runtime::Runtime(int dim, RuntimeConfig cfg) : dim_(dim), cfg_(cfg) {
   if (dim < 1 || dim > kMaxDims) throw InvalidArgument("Runtime: block dim must be 1, 2, or 3");
   if (cfg_.threads < 1) throw InvalidArgument("Runtime: threads must be >= 1");
   if (cfg_.skew_allowance < 0) throw InvalidArgument("Runtime: skew_allowance must be >= 0");
+  if (const char* e = std::getenv("TCG_AUTO_CANDS")) {
+    auto_cands_ = 0;
+    for (const char* c = e; *c; ++c)
+      if (*c >= '0' && *c < '0' + kCand) auto_cands_ |= 1u << (*c - '0');
+    auto_cands_ |= 2u;  // untiled always runs
+  }
   // tiled_auto decisions persisted across processes (like a library autotune
-  // cache): "signature ms_l2 ms_untiled ms_windowed fits_mask" per line.
+  // cache): "signature ms_l2 ms_untiled ms_windowed ms_stream fits_mask" per line.
   if (const char* path = std::getenv("TCG_AUTOTUNE_FILE")) {
     autotune_file_ = path;
     if (FILE* f = std::fopen(path, "r")) {
       unsigned long long sig = 0;
-      float m0 = 0, m1 = 0, m2 = 0;
+      float m0 = 0, m1 = 0, m2 = 0, m3 = 0;
       int fits = 0;
-      while (std::fscanf(f, "%llx %f %f %f %d", &sig, &m0, &m1, &m2, &fits) == 5) {
+      while (std::fscanf(f, "%llx %f %f %f %f %d", &sig, &m0, &m1, &m2, &m3, &fits) == 6) {
         AutoStat& a = auto_[static_cast<uint64_t>(sig)];
-        const float m[kCand] = {m0, m1, m2};
+        const float m[kCand] = {m0, m1, m2, m3};
         for (int c = 0; c < kCand; ++c) {
           a.runs[c] = kAutoRuns;
           a.ms[c] = m[c];
@@ -796,11 +803,20 @@ std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode,
   // candidate twice per chain signature (round robin; the first run of each
   // carries plan construction and lazy module loading) and then keeps the
   // fastest -- they are all bit-exact.
-  int cand = mode.kind == ExecMode::Kind::Untiled ? 1 : mode.kind == ExecMode::Kind::Windowed ? 2 : 0;
+  int cand = mode.kind == ExecMode::Kind::Untiled    ? 1
+             : mode.kind == ExecMode::Kind::Windowed ? 2
+             : mode.kind == ExecMode::Kind::Stream   ? 3
+                                                     : 0;
   AutoStat* as = nullptr;
   bool measure = false;
   if (mode.kind == ExecMode::Kind::TiledAuto) {
-    as = &auto_[chain.signature() ^ mask_hash(*this, t.masked, t.mask, chain.dim)];
+    const uint64_t akey = chain.signature() ^ mask_hash(*this, t.masked, t.mask, chain.dim);
+    auto ait = auto_.find(akey);
+    if (ait == auto_.end()) {
+      ait = auto_.emplace(akey, AutoStat{}).first;
+      for (int c = 0; c < kCand; ++c) ait->second.fits[c] = ((auto_cands_ >> c) & 1u) != 0;
+    }
+    as = &ait->second;
     if (as->ev1) {
       // Resolve the pending measurement (waits for it: only while tuning).
       float ms = 0;
@@ -832,6 +848,9 @@ std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode,
       if (cand == 0) {
         rep.executor = "tiled";
         run_l2(chain, mode, rep, t, vals);
+      } else if (cand == 3) {
+        rep.executor = "stream";
+        run_stream(chain, rep, t, vals);
       } else {
         rep.executor = "windowed";
         run_tiled(chain, mode, rep, t, vals);
@@ -857,26 +876,7 @@ std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode,
   }
   if (use_untiled) {
     rep.executor = "untiled";
-    // Pad sufficiency of untiled execution: every access of the recorded
-    // ranges must stay inside its allocation (the reference's checked
-    // accessor would throw AccessError at run time, kernel_ctx.hpp:58-73).
-    for (const LoopRecord& lp : chain.loops) {
-      if (lp.range.empty()) continue;
-      for (const ArgSpec& a : lp.args) {
-        const Stencil& st = chain.stencil(a.stencil);
-        Point lo{0, 0, 0}, hi{0, 0, 0};
-        for (int d = 0; d < chain.dim; ++d) {
-          lo[d] = mode_reads(a.mode) ? std::min<int64_t>(st.min_offset(d), 0) : 0;
-          hi[d] = mode_reads(a.mode) ? std::max<int64_t>(st.max_offset(d), 0) : 0;
-        }
-        const Range touched = lp.range.dilated(lo, hi);
-        const Range& alloc = t.alloc.at(static_cast<size_t>(a.dataset));
-        if (!alloc.contains(touched))
-          throw AccessError("loop k" + std::to_string(lp.kernel.id) + " (id " + std::to_string(lp.loop_id) +
-                            "), dataset " + fields_[static_cast<size_t>(a.dataset)].name + ": access over " +
-                            touched.to_string() + " outside allocated extent " + alloc.to_string());
-      }
-    }
+    check_pad(chain, t);
     DevChain dc = lower(chain, t);
     std::vector<double> out(static_cast<size_t>(std::max(1, dc.nred)));
     dev.run_untiled(dc, out.data());
@@ -887,6 +887,150 @@ std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode,
   for (size_t i = 0; i < red_src.size(); ++i)
     if (red_src[i] >= 0) all_vals[i] = vals[static_cast<size_t>(red_src[i])];
   return all_vals;
+}
+
+// ---- streaming executor ------------------------------------------------------
+
+std::vector<StreamGeom> Runtime::stream_geoms(const Target& t, bool from_device) {
+  std::vector<StreamGeom> g(t.alloc.size());
+  for (size_t ds = 0; ds < t.alloc.size(); ++ds) {
+    StreamGeom& q = g[ds];
+    q.alloc = t.alloc[ds];
+    if (from_device && !t.dev.empty() && t.dev[ds] >= 0) {
+      const DevView v = device().view(t.dev[ds], false);
+      q.x0 = v.x0;
+      q.y0 = v.y0;
+      q.z0 = v.z0;
+      q.py = v.py;
+      q.pz = v.pz;
+    } else {
+      const Range& a = t.alloc[ds];
+      int64_t lo[3], hi[3];
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = d < a.dim() ? a.start(d) : 0;
+        hi[d] = d < a.dim() ? a.end(d) : 1;
+      }
+      const FieldLayout fl = field_layout(a.dim(), lo, hi);
+      q.x0 = fl.x0;
+      q.y0 = a.dim() >= 2 ? a.start(1) : 0;
+      q.z0 = a.dim() >= 3 ? a.start(2) : 0;
+      q.py = a.dim() >= 2 ? fl.py : 0;
+      q.pz = a.dim() >= 3 ? fl.pz : 0;
+    }
+  }
+  return g;
+}
+
+StreamPlan Runtime::stream_plan_pending(const StreamDevice& sd) {
+  LoopChain chain = take_pending();
+  Target t;
+  for (const FieldRec& f : fields_) {
+    t.dev.push_back(-1);
+    t.alloc.push_back(f.alloc);
+  }
+  return build_stream_plan(chain, stream_geoms(t, false), sd, stream_choice_, nullptr);
+}
+
+void Runtime::run_stream(const LoopChain& chain, ExecutionReport& rep, const Target& t, std::vector<double>& vals) {
+  DeviceExec& dev = device();
+  if (chain.dim < 2) throw PlanError("stream executor: 1D chains are not streamed");
+  check_pad(chain, t);
+  uint64_t key = chain.signature() ^ mask_hash(*this, t.masked, t.mask, chain.dim);
+  for (int f : t.dev) key = (key ^ static_cast<uint64_t>(f + 7)) * 1099511628211ull;
+  {
+    const StreamChoice& c = stream_choice_;
+    const int cv[8] = {c.nt, c.bx, c.by, c.ntx, c.segments, c.max_loops, c.minb, c.prefetch};
+    for (int v : cv) key = (key ^ static_cast<uint64_t>(v + 1000)) * 1099511628211ull;
+  }
+  auto it = stream_plans_.find(key);
+  if (it == stream_plans_.end()) {
+    rep.plan_cache_hit = false;
+    StreamDevice sd;
+    sd.num_sms = dev.info().num_sms;
+    sd.smem_optin = dev.info().smem_optin;
+    auto plan = std::make_shared<StreamPlan>(
+        build_stream_plan(chain, stream_geoms(t, true), sd, stream_choice_, t.masked ? &t.mask : nullptr));
+    ++rep.plan_constructions;
+    rep.plan_seconds += plan->build_seconds;
+    it = stream_plans_.emplace(key, plan).first;
+  } else {
+    rep.plan_cache_hit = true;
+  }
+  const StreamPlan& plan = *it->second;
+  last_stream_plan_ = it->second;
+  size_t nred_total = 0;
+  for (const StreamKernel& k : plan.kernels) nred_total += k.red_op.size();
+  std::vector<uint64_t> buf;
+  size_t red_base = 0;
+  for (const StreamKernel& K : plan.kernels) {
+    if (K.nctas == 0) continue;
+    void* fn = jit_function(K.source, K.hash, K.smem_bytes);
+    const size_t nd = K.dats.size();
+    buf.assign(2 * nd + 3 + static_cast<size_t>(std::max(1, K.nparams)), 0);
+    for (size_t k = 0; k < nd; ++k) {
+      const int f = t.dev.at(static_cast<size_t>(K.dats[k]));
+      if (K.store[k] && K.pingpong[k]) dev.sync_alt(f, K.store_box[k]);
+      const DevView src = dev.view(f, false);
+      buf[k] = reinterpret_cast<uint64_t>(src.base);
+      buf[nd + k] = reinterpret_cast<uint64_t>(K.store[k] && K.pingpong[k] ? dev.view(f, true).base : src.base);
+      if (K.store[k] && !K.pingpong[k]) dev.mark_written(f, K.store_box[k]);
+    }
+    double *part = nullptr, *out = nullptr;
+    unsigned* ticket = nullptr;
+    dev.stream_red_buffers(std::max<size_t>(1, K.red_op.size() * static_cast<size_t>(K.nctas)),
+                           std::max<size_t>(1, nred_total), &part, &out, &ticket);
+    buf[2 * nd] = reinterpret_cast<uint64_t>(part);
+    buf[2 * nd + 1] = reinterpret_cast<uint64_t>(out + red_base);
+    buf[2 * nd + 2] = reinterpret_cast<uint64_t>(ticket);
+    double* prm = reinterpret_cast<double*>(buf.data() + 2 * nd + 3);
+    size_t pi = 0;
+    for (size_t l = K.begin; l < K.end; ++l)
+      for (double v : chain.loops[l].kernel.fn.params) prm[pi++] = v;
+    dev.launch_stream(fn, K.nctas, K.nt, K.smem_bytes, buf.data(), buf.size() * sizeof(uint64_t));
+    for (size_t k = 0; k < nd; ++k)
+      if (K.store[k] && K.pingpong[k]) dev.commit_alt(t.dev.at(static_cast<size_t>(K.dats[k])), K.store_box[k]);
+    red_base += K.red_op.size();
+    rep.ctas += K.nctas;
+    rep.computed_points += K.computed_points;
+    rep.subchains += 1;
+    rep.tile_sizes[0] = K.tile[0];
+    if (chain.dim == 3) rep.tile_sizes[1] = K.tile[1];
+    rep.cta_grid[0] = K.grid[0];
+    rep.cta_grid[1] = K.grid[1];
+    rep.cta_grid[2] = K.grid[2];
+  }
+  rep.tiles_executed += rep.ctas;
+  if (nred_total > 0) {
+    double *part = nullptr, *out = nullptr;
+    unsigned* ticket = nullptr;
+    dev.stream_red_buffers(1, nred_total, &part, &out, &ticket);
+    std::vector<double> r(nred_total);
+    dev.read_device(r.data(), out, nred_total);
+    for (size_t i = 0; i < nred_total; ++i) vals.at(i) = r[i];
+  }
+}
+
+void Runtime::check_pad(const LoopChain& chain, const Target& t) const {
+  // Pad sufficiency of untiled execution: every access of the recorded
+  // ranges must stay inside its allocation (the reference's checked
+  // accessor would throw AccessError at run time, kernel_ctx.hpp:58-73).
+  for (const LoopRecord& lp : chain.loops) {
+    if (lp.range.empty()) continue;
+    for (const ArgSpec& a : lp.args) {
+      const Stencil& st = chain.stencil(a.stencil);
+      Point lo{0, 0, 0}, hi{0, 0, 0};
+      for (int d = 0; d < chain.dim; ++d) {
+        lo[d] = mode_reads(a.mode) ? std::min<int64_t>(st.min_offset(d), 0) : 0;
+        hi[d] = mode_reads(a.mode) ? std::max<int64_t>(st.max_offset(d), 0) : 0;
+      }
+      const Range touched = lp.range.dilated(lo, hi);
+      const Range& alloc = t.alloc.at(static_cast<size_t>(a.dataset));
+      if (!alloc.contains(touched))
+        throw AccessError("loop k" + std::to_string(lp.kernel.id) + " (id " + std::to_string(lp.loop_id) +
+                          "), dataset " + fields_[static_cast<size_t>(a.dataset)].name + ": access over " +
+                          touched.to_string() + " outside allocated extent " + alloc.to_string());
+    }
+  }
 }
 
 ExecutionReport Runtime::execute_chain(LoopChain chain, const ExecMode& mode) {
@@ -914,8 +1058,8 @@ void Runtime::save_autotune(AutoStat& as) {
   if (FILE* f = std::fopen(autotune_file_.c_str(), "w")) {
     for (const auto& [sig, a] : auto_)
       if (a.saved)
-        std::fprintf(f, "%llx %.6f %.6f %.6f %d\n", static_cast<unsigned long long>(sig), a.ms[0], a.ms[1], a.ms[2],
-                     (a.fits[0] ? 1 : 0) | (a.fits[1] ? 2 : 0) | (a.fits[2] ? 4 : 0));
+        std::fprintf(f, "%llx %.6f %.6f %.6f %.6f %d\n", static_cast<unsigned long long>(sig), a.ms[0], a.ms[1],
+                     a.ms[2], a.ms[3], (a.fits[0] ? 1 : 0) | (a.fits[1] ? 2 : 0) | (a.fits[2] ? 4 : 0) | (a.fits[3] ? 8 : 0));
     std::fclose(f);
   }
 }

@@ -18,6 +18,7 @@
 #include "tcg_exec.hpp"
 #include "tcg_gpuplan.hpp"
 #include "tcg_plan.hpp"
+#include "tcg_stream.hpp"
 
 namespace tcg {
 
@@ -35,13 +36,16 @@ struct ExecMode {
   // (tile_sizes as in the reference; 0 = GPU sizer). Windowed is the
   // shared-memory windowed executor (tile_sizes = column block / stream tile
   // upper bounds; 0 = sizer).
-  enum class Kind : uint8_t { Untiled = 0, Tiled = 1, TiledAuto = 2, Windowed = 3 };
+  // Stream is the fused streaming executor (generated per chain, DESIGN.md
+  // §3.2); TiledAuto times untiled and stream per chain signature.
+  enum class Kind : uint8_t { Untiled = 0, Tiled = 1, TiledAuto = 2, Windowed = 3, Stream = 4 };
   Kind kind = Kind::Untiled;
   std::array<int64_t, kMaxDims> tile_sizes{0, 0, 0};
   static ExecMode untiled() { return {}; }
   static ExecMode tiled(const std::array<int64_t, kMaxDims>& ts) { return {Kind::Tiled, ts}; }
   static ExecMode tiled_auto() { return {Kind::TiledAuto, {0, 0, 0}}; }
   static ExecMode windowed(const std::array<int64_t, kMaxDims>& ts) { return {Kind::Windowed, ts}; }
+  static ExecMode stream() { return {Kind::Stream, {0, 0, 0}}; }
 };
 
 struct LoopExecStats {
@@ -139,6 +143,12 @@ class Runtime {
   const std::vector<Stencil>& stencils() const { return stencils_; }
   const ExecutionReport& last_report() const { return last_report_; }
   std::shared_ptr<const GpuTiledPlan> last_gpu_plan() const { return last_gpu_plan_; }
+  std::shared_ptr<const StreamPlan> last_stream_plan() const { return last_stream_plan_; }
+  void set_stream_choice(const StreamChoice& c) { stream_choice_ = c; }
+  const StreamChoice& stream_choice() const { return stream_choice_; }
+  // Host-only: the streaming plan (with generated sources) of the pending
+  // chain, consumed; field geometry from the device layout rule.
+  StreamPlan stream_plan_pending(const StreamDevice& sd);
   PlanCache& plan_cache() { return plan_cache_; }
   int64_t gpu_plan_constructions() const { return gpu_plan_builds_; }
   DeviceExec& device();
@@ -194,6 +204,12 @@ class Runtime {
                  std::vector<double>& vals);
   void run_l2(const LoopChain& chain, const ExecMode& mode, ExecutionReport& rep, const Target& t,
               std::vector<double>& vals);
+  void run_stream(const LoopChain& chain, ExecutionReport& rep, const Target& t, std::vector<double>& vals);
+  void check_pad(const LoopChain& chain, const Target& t) const;
+  std::vector<StreamGeom> stream_geoms(const Target& t, bool from_device);
+  StreamChoice stream_choice_;
+  std::map<uint64_t, std::shared_ptr<const StreamPlan>> stream_plans_;
+  std::shared_ptr<const StreamPlan> last_stream_plan_;
   struct L2Sub {
     size_t begin, end;  // loops [begin, end)
     int64_t ts;         // slowest-dim tile size
@@ -226,12 +242,15 @@ class Runtime {
   // untiled executor (both bit-exact); later flushes use the faster one.
   // tiled_auto: per chain signature, device time of each executor candidate
   // (0 L2-tiled, 1 untiled, 2 windowed); all bit-exact, the fastest is kept.
-  static constexpr int kCand = 3;
+  // Candidates: 0 L2-tiled, 1 untiled, 2 windowed, 3 stream; enabled by
+  // auto_cands_ (default untiled + stream; TCG_AUTO_CANDS=0,1,2,3).
+  static constexpr int kCand = 4;
   static constexpr int kAutoRuns = 3;  // timed runs per candidate (min kept)
+  unsigned auto_cands_ = 0xA;
   struct AutoStat {
-    int runs[kCand] = {0, 0, 0};
-    float ms[kCand] = {1e30f, 1e30f, 1e30f};
-    bool fits[kCand] = {true, true, true};
+    int runs[kCand] = {0, 0, 0, 0};
+    float ms[kCand] = {1e30f, 1e30f, 1e30f, 1e30f};
+    bool fits[kCand] = {true, true, true, true};
     void* ev0 = nullptr;
     void* ev1 = nullptr;
     int pending = -1;    // candidate being timed

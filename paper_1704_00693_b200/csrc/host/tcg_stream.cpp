@@ -1,0 +1,1297 @@
+// Streaming fused-chain executor: dependency analysis, sizing and CUDA code
+// generation (see tcg_stream.hpp for the design).
+#include "tcg_stream.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <set>
+#include <sstream>
+
+namespace tcg {
+namespace {
+
+constexpr int64_t kNone = -(int64_t{1} << 60);
+
+// One dataset version: the state of a dataset after loop `prod` wrote it
+// (prod = -1: the state the chain starts from, read from HBM).
+struct SVer {
+  int slot = -1;
+  int prod = -1;
+  bool needed = false;
+  int64_t need[3][2] = {{kNone, kNone}, {kNone, kNone}, {kNone, kNone}};
+  bool pass_only = true;     // input read only to pass unchanged points through
+  std::vector<int> pass_by;  // loops passing it through
+  bool store = false;
+  // schedule
+  int64_t lag = 0;
+  int dr = 1;        // register ring depth (ages 0 .. dr-1)
+  int ds = 0;        // shared-memory ring depth (0: none)
+  int64_t sbase = 0; // shared-memory ring offset (rows)
+  bool tma = false;  // input rows arrive by bulk copy into the shared ring
+};
+
+struct SRead {
+  int v = -1;
+  int arg = -1;
+  int64_t off[3] = {0, 0, 0};
+  bool pass = false;  // pass-through of a point outside the writer's range
+};
+
+struct SLoop {
+  int64_t lag = 0;
+  std::vector<int> vin, vout, prev;  // per argument, -1 = none
+  std::vector<SRead> reads;
+  bool needed = false;
+  int64_t need[3][2] = {{kNone, kNone}, {kNone, kNone}, {kNone, kNone}};
+};
+
+struct Analysis {
+  int dim = 2, s = 1;
+  std::vector<SVer> vers;
+  std::vector<SLoop> loops;
+  std::vector<DatasetId> dats;  // slot -> dataset
+  std::vector<int> input_ver;   // slot -> input version
+  std::vector<int> final_ver;   // slot -> last version written (-1 none)
+  std::vector<Range> whull;     // slot -> hull of the loops writing it
+  std::vector<Range> first_w;   // slot -> range of the first writer
+  std::vector<uint8_t> all_w_in_first;
+  Range T, H;
+  bool any_out = false;
+  int64_t E[3][2] = {};
+};
+
+Range hull_or(const Range& a, bool a_set, const Range& b) { return a_set ? a.hull(b) : b; }
+
+Analysis analyze(const LoopChain& ch, const std::vector<DatasetId>& nostore = {}) {
+  Analysis A;
+  A.dim = ch.dim;
+  A.s = ch.dim - 1;
+  const int s = A.s;
+  // Touched hull T: every point any loop reads or writes.
+  bool tset = false;
+  for (const LoopRecord& lp : ch.loops) {
+    A.T = hull_or(A.T, tset, lp.range);
+    tset = true;
+    for (const ArgSpec& a : lp.args)
+      if (mode_reads(a.mode)) {
+        const Stencil& st = ch.stencil(a.stencil);
+        Point lo{0, 0, 0}, hi{0, 0, 0};
+        for (int d = 0; d < ch.dim; ++d) {
+          lo[d] = std::min<int64_t>(st.min_offset(d), 0);
+          hi[d] = std::max<int64_t>(st.max_offset(d), 0);
+        }
+        A.T = A.T.hull(lp.range.dilated(lo, hi));
+      }
+  }
+  std::map<DatasetId, int> slot_of;
+  auto slot = [&](DatasetId ds) {
+    auto it = slot_of.find(ds);
+    if (it != slot_of.end()) return it->second;
+    const int k = static_cast<int>(A.dats.size());
+    slot_of[ds] = k;
+    A.dats.push_back(ds);
+    A.input_ver.push_back(-1);
+    A.final_ver.push_back(-1);
+    A.whull.push_back(Range(ch.dim));
+    A.first_w.push_back(Range(ch.dim));
+    A.all_w_in_first.push_back(1);
+    return k;
+  };
+  std::vector<int> cur;
+  auto version_of = [&](int k) {
+    if (static_cast<size_t>(k) >= cur.size()) cur.resize(static_cast<size_t>(k) + 1, -1);
+    if (cur[static_cast<size_t>(k)] >= 0) return cur[static_cast<size_t>(k)];
+    if (A.input_ver[static_cast<size_t>(k)] < 0) {
+      SVer v;
+      v.slot = k;
+      A.input_ver[static_cast<size_t>(k)] = static_cast<int>(A.vers.size());
+      A.vers.push_back(v);
+    }
+    return A.input_ver[static_cast<size_t>(k)];
+  };
+  // Versions, reads and pass-through edges.
+  for (size_t l = 0; l < ch.loops.size(); ++l) {
+    const LoopRecord& lp = ch.loops[l];
+    SLoop L;
+    const size_t na = lp.args.size();
+    L.vin.assign(na, -1);
+    L.vout.assign(na, -1);
+    L.prev.assign(na, -1);
+    std::vector<int> ks(na);
+    for (size_t a = 0; a < na; ++a) ks[a] = slot(lp.args[a].dataset);
+    for (size_t a = 0; a < na; ++a)
+      for (size_t b = a + 1; b < na; ++b)
+        if (ks[a] == ks[b] && mode_writes(lp.args[a].mode) && mode_writes(lp.args[b].mode))
+          throw PlanError("stream executor: loop writes one dataset through two arguments");
+    for (size_t a = 0; a < na; ++a) {
+      if (!mode_reads(lp.args[a].mode)) continue;
+      const int v = version_of(ks[a]);
+      L.vin[a] = v;
+      if (A.vers[static_cast<size_t>(v)].prod < 0) A.vers[static_cast<size_t>(v)].pass_only = false;
+      const Stencil& st = ch.stencil(lp.args[a].stencil);
+      for (const Point& p : st.points()) {
+        SRead r;
+        r.v = v;
+        r.arg = static_cast<int>(a);
+        for (int d = 0; d < 3; ++d) r.off[d] = p[d];
+        L.reads.push_back(r);
+      }
+    }
+    const bool pass = !lp.range.contains(A.T);
+    for (size_t a = 0; a < na; ++a) {
+      if (!mode_writes(lp.args[a].mode)) continue;
+      const int k = ks[a];
+      if (pass) {
+        const int pv = version_of(k);
+        L.prev[a] = pv;
+        SRead r;
+        r.v = pv;
+        r.arg = static_cast<int>(a);
+        r.pass = true;
+        L.reads.push_back(r);
+        A.vers[static_cast<size_t>(pv)].pass_by.push_back(static_cast<int>(l));
+      }
+      SVer nv;
+      nv.slot = k;
+      nv.prod = static_cast<int>(l);
+      L.vout[a] = static_cast<int>(A.vers.size());
+      A.vers.push_back(nv);
+      const bool first = A.final_ver[static_cast<size_t>(k)] < 0;
+      A.whull[static_cast<size_t>(k)] = first ? lp.range : A.whull[static_cast<size_t>(k)].hull(lp.range);
+      if (first)
+        A.first_w[static_cast<size_t>(k)] = lp.range;
+      else if (!A.first_w[static_cast<size_t>(k)].contains(lp.range))
+        A.all_w_in_first[static_cast<size_t>(k)] = 0;
+      A.final_ver[static_cast<size_t>(k)] = L.vout[a];
+    }
+    for (size_t a = 0; a < na; ++a)
+      if (L.vout[a] >= 0) {
+        if (static_cast<size_t>(ks[a]) >= cur.size()) cur.resize(static_cast<size_t>(ks[a]) + 1, -1);
+        cur[static_cast<size_t>(ks[a])] = L.vout[a];
+      }
+    A.loops.push_back(std::move(L));
+  }
+  // Stored versions: the final version of every written dataset.
+  for (size_t k = 0; k < A.dats.size(); ++k)
+    if (A.final_ver[k] >= 0 && std::find(nostore.begin(), nostore.end(), A.dats[k]) == nostore.end())
+      A.vers[static_cast<size_t>(A.final_ver[k])].store = true;
+  // Backward walk: the extension each version must be correct over, beyond
+  // the CTA's owned box, for the stored outputs and reductions to be exact
+  // (the overlapped-tile extension of construct_rank_plan, dist.cpp:268-310).
+  for (SVer& v : A.vers)
+    if (v.store) {
+      v.needed = true;
+      for (int d = 0; d < 3; ++d) v.need[d][0] = v.need[d][1] = 0;
+    }
+  for (size_t li = ch.loops.size(); li-- > 0;) {
+    SLoop& L = A.loops[li];
+    const LoopRecord& lp = ch.loops[li];
+    if (lp.reduction) {
+      L.needed = true;
+      for (int d = 0; d < 3; ++d) L.need[d][0] = L.need[d][1] = 0;
+    }
+    for (int v : L.vout)
+      if (v >= 0 && A.vers[static_cast<size_t>(v)].needed) {
+        L.needed = true;
+        for (int d = 0; d < 3; ++d)
+          for (int e = 0; e < 2; ++e) L.need[d][e] = std::max(L.need[d][e], A.vers[static_cast<size_t>(v)].need[d][e]);
+      }
+    if (!L.needed) continue;
+    for (const SRead& r : L.reads) {
+      SVer& v = A.vers[static_cast<size_t>(r.v)];
+      v.needed = true;
+      for (int d = 0; d < 3; ++d) {
+        v.need[d][0] = std::max(v.need[d][0], L.need[d][0] - r.off[d]);
+        v.need[d][1] = std::max(v.need[d][1], L.need[d][1] + r.off[d]);
+      }
+    }
+  }
+  // Extension and the owned hull H (stored write hulls + reducing ranges).
+  for (int d = 0; d < 3; ++d) A.E[d][0] = A.E[d][1] = 0;
+  for (const SVer& v : A.vers)
+    if (v.needed)
+      for (int d = 0; d < A.dim; ++d)
+        for (int e = 0; e < 2; ++e) A.E[d][e] = std::max(A.E[d][e], v.need[d][e]);
+  bool hset = false;
+  for (size_t k = 0; k < A.dats.size(); ++k)
+    if (A.final_ver[k] >= 0 && A.vers[static_cast<size_t>(A.final_ver[k])].store) {
+      A.H = hull_or(A.H, hset, A.whull[k]);
+      hset = true;
+    }
+  for (size_t li = 0; li < ch.loops.size(); ++li)
+    if (ch.loops[li].reduction) {
+      A.H = hull_or(A.H, hset, ch.loops[li].range);
+      hset = true;
+    }
+  A.any_out = hset && !A.H.empty();
+  return A;
+}
+
+// ---------------------------------------------------------------- schedule
+// Each thread owns a bx x by block of cross-section points (by = 1 in 2D).
+// A read whose target point lies in another thread's block goes through a
+// shared-memory ring and must target a row produced in an earlier step (age
+// >= 1), so one barrier per step orders every producer before its readers.
+// 2D: a thread's points are strided by the CTA width (x = x0 + tid + j*nt),
+// so every in-plane neighbour belongs to another thread; 3D: a contiguous
+// bx x by block (y neighbours inside it come from registers).
+struct Block {
+  int bx = 1, by = 1;
+  bool strided = false;
+  bool own_smem = false;  // reads of shared versions at age >= 1 use the smem ring (2D)
+};
+
+struct Sched {
+  std::vector<SVer> vers;
+  std::vector<int64_t> lag;  // per loop
+  int64_t lmax = 0;
+  int reg_doubles = 0;  // register-ring doubles per point
+  int smem_rows = 0;    // shared-memory ring rows (planes) over all versions
+  int rx = 0, ry = 0;   // in-plane reach of shared-memory reads
+  int la = 1;           // bulk-copy lookahead (steps between a row's copy and its first use)
+  int unroll = 1;       // step-loop unroll: every ring depth divides it
+  int nbar = 0;         // mbarrier ring (0: no bulk-copied inputs)
+  int ntma = 0;         // bulk-copied input versions
+};
+
+int pow2ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+bool in_block(const Block& b, const SRead& r, int dim, int jx, int jy) {
+  if (r.pass) return true;
+  if (b.strided && r.off[0] != 0) return false;
+  const int tx = jx + static_cast<int>(r.off[0]);
+  const int ty = jy + (dim == 3 ? static_cast<int>(r.off[1]) : 0);
+  return tx >= 0 && tx < b.bx && ty >= 0 && ty < b.by;
+}
+
+bool crosses(const Block& b, const SRead& r, int dim) {
+  for (int jy = 0; jy < b.by; ++jy)
+    for (int jx = 0; jx < b.bx; ++jx)
+      if (!in_block(b, r, dim, jx, jy)) return true;
+  return false;
+}
+
+Sched schedule(const Analysis& A, const Block& B, int la) {
+  Sched S;
+  S.vers = A.vers;
+  const int s = A.s;
+  std::vector<uint8_t> shared(S.vers.size(), 0);
+  for (const SLoop& L : A.loops)
+    if (L.needed)
+      for (const SRead& r : L.reads)
+        if (crosses(B, r, A.dim)) shared[static_cast<size_t>(r.v)] = 1;
+  S.lag.assign(A.loops.size(), 0);
+  for (size_t li = 0; li < A.loops.size(); ++li) {
+    const SLoop& L = A.loops[li];
+    if (!L.needed) continue;
+    int64_t lag = 0;
+    for (const SRead& r : L.reads) {
+      const SVer& v = S.vers[static_cast<size_t>(r.v)];
+      if (v.prod >= 0) lag = std::max(lag, v.lag + r.off[s] + (crosses(B, r, A.dim) ? 1 : 0));
+    }
+    S.lag[li] = lag;
+    for (int v : L.vout)
+      if (v >= 0) S.vers[static_cast<size_t>(v)].lag = lag;
+  }
+  // Inputs: rows read in full arrive by bulk copy `la` steps before their
+  // first use; pass-through-only inputs (a few boundary points) by
+  // predicated register loads one step ahead.
+  for (size_t vi = 0; vi < S.vers.size(); ++vi) {
+    SVer& v = S.vers[vi];
+    if (v.prod >= 0 || !v.needed) continue;
+    v.tma = !v.pass_only;
+    const int lead = v.tma ? la : 1;
+    int64_t lag = int64_t{1} << 40;
+    for (size_t li = 0; li < A.loops.size(); ++li) {
+      if (!A.loops[li].needed) continue;
+      for (const SRead& r : A.loops[li].reads)
+        if (r.v == static_cast<int>(vi)) lag = std::min(lag, S.lag[li] - r.off[s] - lead);
+    }
+    v.lag = lag;
+  }
+  int64_t lmin = int64_t{1} << 40;
+  for (size_t li = 0; li < A.loops.size(); ++li)
+    if (A.loops[li].needed) lmin = std::min(lmin, S.lag[li]);
+  for (const SVer& v : S.vers)
+    if (v.needed) lmin = std::min(lmin, v.lag);
+  if (lmin == (int64_t{1} << 40)) lmin = 0;
+  for (int64_t& l : S.lag) l -= lmin;
+  for (SVer& v : S.vers) v.lag -= lmin;
+  S.lmax = 0;
+  for (size_t li = 0; li < A.loops.size(); ++li)
+    if (A.loops[li].needed) S.lmax = std::max(S.lmax, S.lag[li]);
+  for (const SVer& v : S.vers)
+    if (v.needed) S.lmax = std::max(S.lmax, v.lag);
+  // Ring depths per read source.
+  for (SVer& v : S.vers) {
+    v.dr = 1;
+    v.ds = 0;
+  }
+  for (size_t li = 0; li < A.loops.size(); ++li) {
+    const SLoop& L = A.loops[li];
+    if (!L.needed) continue;
+    for (const SRead& r : L.reads) {
+      SVer& v = S.vers[static_cast<size_t>(r.v)];
+      const int64_t age = S.lag[li] - r.off[s] - v.lag;
+      if (age < 0) throw PlanError("stream executor: internal lag error");
+      for (int jy = 0; jy < B.by; ++jy)
+        for (int jx = 0; jx < B.bx; ++jx) {
+          const bool blk = in_block(B, r, A.dim, jx, jy);
+          const bool sm = v.tma || !blk || (shared[static_cast<size_t>(r.v)] && B.own_smem && age >= 1);
+          if (sm) {
+            if (age < 1) throw PlanError("stream executor: internal age error");
+            v.ds = std::max<int>(v.ds, static_cast<int>(age) + 1);
+            if (!blk) {
+              S.rx = std::max(S.rx, std::abs(static_cast<int>(r.off[0])));
+              if (A.dim == 3) S.ry = std::max(S.ry, std::abs(static_cast<int>(r.off[1])));
+            }
+          } else {
+            v.dr = std::max<int>(v.dr, static_cast<int>(age) + 1);
+          }
+        }
+    }
+  }
+  // Ring depths padded to powers of two; the step loop is unrolled by the
+  // largest, so every ring slot is a compile-time index in every phase.
+  S.la = la;
+  S.unroll = 1;
+  S.ntma = 0;
+  for (SVer& v : S.vers) {
+    if (!v.needed) continue;
+    if (v.tma) {
+      v.dr = 0;
+      v.ds = std::max(v.ds, la + 1);
+      ++S.ntma;
+    }
+    v.dr = v.dr ? pow2ceil(v.dr) : 0;
+    if (v.ds > 0) v.ds = pow2ceil(v.ds);
+    S.unroll = std::max({S.unroll, v.dr, v.ds});
+  }
+  if (S.ntma) {
+    S.nbar = pow2ceil(la + 1);
+    S.unroll = std::max(S.unroll, S.nbar);
+    S.rx = std::max(S.rx, 2);  // even-rounded copy ends overrun the tile by one
+  }
+  S.reg_doubles = 0;
+  S.smem_rows = 0;
+  int64_t off = 0;
+  for (SVer& v : S.vers) {
+    if (!v.needed) continue;
+    S.reg_doubles += v.dr;
+    S.smem_rows += v.ds;
+    v.sbase = off;  // in rows; scaled by the plane size in the sizer
+    off += v.ds;
+  }
+  return S;
+}
+
+// ---------------------------------------------------------------- shape
+struct Shape {
+  Block blk;
+  int nt = 256, ntx = 256;
+  int tx = 512, ty = 1;
+  int rx = 0, ry = 0, spx = 0;
+  int64_t sp = 0;
+  int64_t exl = 0, eyl = 0;  // tile origin offsets (x includes the even alignment)
+  int64_t wox = 0, woy = 1;
+  int64_t nxt = 1, nyt = 1, ns = 1;
+  int minb = 1;
+  int prefetch = 0;
+  int regs = 0;
+  int64_t smem_bytes = 0;
+  double cost = 0;   // relative time per owned point (sizer)
+  double est_s = 0;  // estimated kernel seconds (sub-chain split)
+};
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+double env_dbl(const char* name, double dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atof(e) : dflt;
+}
+
+int est_regs(const Sched& sc, int P, int nloops) { return 2 * P * sc.reg_doubles + 6 * P + 44 + nloops / 4; }
+
+// Picks the thread-block shape and CTA grid of one kernel (or applies the
+// overrides in `c`); fills `sc` with the matching schedule. Throws PlanError
+// when nothing fits.
+Shape size_kernel(const Analysis& A, const LoopChain& ch, const StreamDevice& dev, const StreamChoice& c, Sched& sc) {
+  const int64_t hx = A.H.extent(0), hy = A.dim == 3 ? A.H.extent(1) : 1, hs = A.H.extent(A.s);
+  const std::vector<int> nts = c.nt ? std::vector<int>{c.nt} : std::vector<int>{64, 128, 192, 256, 384, 512};
+  const std::vector<int> bxs = c.bx ? std::vector<int>{c.bx} : std::vector<int>{1, 2, 4};
+  const std::vector<int> bys =
+      A.dim == 2 ? std::vector<int>{1} : (c.by ? std::vector<int>{c.by} : std::vector<int>{1, 2, 4});
+  const std::vector<int> ntxs = A.dim == 2 ? std::vector<int>{0} : (c.ntx ? std::vector<int>{c.ntx} : std::vector<int>{8, 16, 32});
+  int nloops = 0;
+  for (const SLoop& L : A.loops) nloops += L.needed ? 1 : 0;
+  const double lat_k = env_dbl("TCG_STREAM_LAT", 6.0);
+  const int la = env_int("TCG_STREAM_LOOKAHEAD", 2);
+  Shape best;
+  Sched best_sc;
+  best.cost = 1e300;
+  std::map<std::pair<int, int>, Sched> scache;
+  for (int bx : bxs)
+    for (int by : bys) {
+      Block B;
+      B.bx = bx;
+      B.by = by;
+      B.own_smem = A.dim == 2;
+      B.strided = A.dim == 2;
+      auto it = scache.find({bx, by});
+      if (it == scache.end()) it = scache.emplace(std::make_pair(bx, by), schedule(A, B, la)).first;
+      const Sched& S0 = it->second;
+      for (int nt : nts)
+        for (int ntx0 : ntxs) {
+          Shape S;
+          S.blk = B;
+          S.nt = nt;
+          S.ntx = A.dim == 2 ? nt : ntx0;
+          if (nt % S.ntx) continue;
+          const int P = bx * by;
+          if (P > 16) continue;
+          S.tx = S.ntx * bx;
+          S.ty = A.dim == 2 ? 1 : (nt / S.ntx) * by;
+          const int align = ((A.dim == 3 && bx > 1) || S0.ntma) ? 1 : 0;
+          S.exl = A.E[0][0] + align;
+          S.wox = S.tx - A.E[0][0] - A.E[0][1] - align;
+          if (align) S.wox &= ~int64_t{1};
+          S.eyl = A.dim == 3 ? A.E[1][0] : 0;
+          S.woy = A.dim == 2 ? 1 : S.ty - A.E[1][0] - A.E[1][1];
+          if (S.wox <= 0 || S.woy <= 0) continue;
+          S.regs = est_regs(S0, P, nloops);
+          if (S.regs > 255) continue;
+          S.rx = (A.dim == 2 && !S0.ntma) ? S0.rx : (S0.rx + 1) & ~1;
+          S.ry = S0.ry;
+          S.spx = S.tx + 2 * S.rx;
+          S.sp = static_cast<int64_t>(S.spx) * (S.ty + 2 * S.ry);
+          S.smem_bytes = std::max<int64_t>(S0.smem_rows * S.sp, 64) * 8;
+          if (S.smem_bytes > dev.smem_optin) continue;
+          S.nxt = (hx + S.wox - 1) / S.wox;
+          S.nyt = A.dim == 2 ? 1 : (hy + S.woy - 1) / S.woy;
+          const int rpt = (S.regs + 7) / 8 * 8;
+          int cps = static_cast<int>(dev.regs_per_sm / (static_cast<int64_t>(rpt) * nt));
+          cps = std::min<int>(cps, static_cast<int>(228 * 1024 / (S.smem_bytes + 1024)));
+          cps = std::min(cps, 2048 / nt);
+          cps = std::min(cps, 32);
+          if (c.minb) cps = std::min(cps, c.minb);
+          if (cps < 1) continue;
+          const double red = static_cast<double>(S.nxt * S.tx) * static_cast<double>(S.nyt * S.ty) /
+                             (static_cast<double>(hx) * static_cast<double>(hy));
+          const double warps = cps * nt / 32.0;
+          const double lat = 1.0 + lat_k / (warps * std::min(P, 4));
+          S.cost = red * lat;
+          S.minb = cps;
+          if (S.cost < best.cost) {
+            best = S;
+            best_sc = S0;
+          }
+        }
+    }
+  if (best.cost >= 1e300) throw PlanError("stream executor: no thread-block shape fits the chain");
+  Shape S = best;
+  sc = best_sc;
+  const int64_t warm = sc.lmax + A.E[A.s][0] + A.E[A.s][1];
+  if (c.segments > 0) {
+    S.ns = c.segments;
+  } else {
+    const int64_t slots = static_cast<int64_t>(dev.num_sms) * S.minb;
+    const int64_t tiles = S.nxt * S.nyt;
+    S.ns = std::max<int64_t>(1, slots / tiles);
+    // Whole waves: round the CTA count to a multiple of the resident slots.
+    if (tiles * S.ns < slots) S.ns = std::max<int64_t>(1, (slots + tiles - 1) / tiles);
+    const int64_t min_len = std::max<int64_t>(8, 4 * warm);
+    S.ns = std::max<int64_t>(1, std::min<int64_t>(S.ns, hs / min_len));
+  }
+  S.ns = std::max<int64_t>(1, std::min<int64_t>(S.ns, hs));
+  S.prefetch = c.prefetch >= 0 ? c.prefetch : 0;
+  // Time estimate (sub-chain split): compute at a sustained rate of
+  // cell-updates per SM clock, HBM at the copy rate; whichever is larger.
+  const double red_s = 1.0 + static_cast<double>(S.ns) * static_cast<double>(warm) / static_cast<double>(std::max<int64_t>(1, hs));
+  const double pts = static_cast<double>(A.H.volume());
+  const double red_xy = static_cast<double>(S.nxt * S.tx) * static_cast<double>(S.nyt * S.ty) /
+                        (static_cast<double>(hx) * static_cast<double>(hy));
+  const double cu_clk = env_dbl("TCG_STREAM_CU_PER_CLK", 1.5);
+  const double t_comp = nloops * pts * red_xy * red_s / (cu_clk * dev.num_sms * 1.9e9);
+  double in_b = 0, out_b = 0;
+  for (const SVer& v : sc.vers)
+    if (v.needed && v.prod < 0) in_b += v.pass_only ? 0.5 : 8.0;
+  for (const SVer& v : sc.vers)
+    if (v.store) out_b += 8.0;
+  const double t_dram = (in_b * (1.0 + 0.5 * (red_xy - 1.0)) + out_b) * pts * red_s / 6.2e12;
+  S.est_s = std::max(t_comp, t_dram) * S.cost / red_xy + 4e-6;
+  (void)ch;
+  return S;
+}
+
+// ---------------------------------------------------------------- codegen
+std::string fmt_L(int64_t v) { return std::to_string(v) + "LL"; }
+
+struct Gen {
+  const LoopChain& ch;
+  const Analysis& A;
+  const Sched& Sc;
+  const Shape& S;
+  std::vector<std::array<int64_t, 4>> boxes;
+  std::set<std::pair<int, int64_t>> rings;  // (version, age) smem ring pointers used
+  struct GC {
+    int64_t x0, y0, z0, py, pz;
+    Range alloc;
+  };
+  std::vector<GC> gcs;
+  std::vector<int> slot_gc;
+
+  int box_id(const Range& r) {
+    const int64_t big = int64_t{1} << 30;
+    std::array<int64_t, 4> b{r.start(0), r.end(0), A.dim == 3 ? r.start(1) : -big, A.dim == 3 ? r.end(1) : big};
+    for (size_t i = 0; i < boxes.size(); ++i)
+      if (boxes[i] == b) return static_cast<int>(i);
+    boxes.push_back(b);
+    return static_cast<int>(boxes.size()) - 1;
+  }
+  int P() const { return S.blk.bx * S.blk.by; }
+  int jx(int j) const { return j % S.blk.bx; }
+  int jy(int j) const { return j / S.blk.bx; }
+  int xstep() const { return S.blk.strided ? S.nt : 1; }
+  // Offsets of point j from the thread's first point: in the tile (smem,
+  // padded row pitch spx) and in a dataset (row pitch py).
+  int64_t sm_off(int j) const { return static_cast<int64_t>(jx(j)) * xstep() + static_cast<int64_t>(jy(j)) * S.spx; }
+  int64_t g_off(const GC& q, int j) const {
+    return static_cast<int64_t>(jx(j)) * xstep() + (A.dim == 3 ? static_cast<int64_t>(jy(j)) * q.py : 0);
+  }
+  int64_t s_lo(const Range& r) const { return r.start(A.s); }
+  int64_t s_hi(const Range& r) const { return r.end(A.s); }
+  bool is_shared(int v) const { return Sc.vers[static_cast<size_t>(v)].ds > 0; }
+  std::string ring(int v, int64_t age) {
+    rings.insert({v, age});
+    return "rs" + std::to_string(v) + "_" + std::to_string(age);
+  }
+  // Expression reading version r.v at r's offset for point j of loop li in
+  // unroll phase u (ring slots are static: (u - age) mod depth).
+  std::string read_expr(size_t li, const SRead& r, int j, int u) {
+    const SVer& v = Sc.vers[static_cast<size_t>(r.v)];
+    const int64_t age = Sc.lag[li] - r.off[A.s] - v.lag;
+    const int ox = r.pass ? 0 : static_cast<int>(r.off[0]);
+    const int oy = r.pass ? 0 : (A.dim == 3 ? static_cast<int>(r.off[1]) : 0);
+    const bool blk = in_block(S.blk, r, A.dim, jx(j), jy(j));
+    const bool sm = v.tma || !blk || (is_shared(r.v) && S.blk.own_smem && age >= 1);
+    if (!sm) {
+      const int tj = (jy(j) + oy) * S.blk.bx + (jx(j) + ox);
+      return "V" + std::to_string(r.v) + "[" + std::to_string(reg_slot(r.v, u, age)) + "][" + std::to_string(tj) + "]";
+    }
+    return "smp[" + std::to_string(sm_slot_off(r.v, u, age) + sm_off(j) + ox + static_cast<int64_t>(oy) * S.spx) + "]";
+  }
+  int reg_slot(int v, int u, int64_t age) const {
+    const int d = Sc.vers[static_cast<size_t>(v)].dr;
+    return static_cast<int>(((u - age) % d + d) % d);
+  }
+  int64_t sm_slot_off(int v, int u, int64_t age) const {
+    const SVer& sv = Sc.vers[static_cast<size_t>(v)];
+    const int64_t sl = ((u - age) % sv.ds + sv.ds) % sv.ds;
+    return (sv.sbase + sl) * S.sp;
+  }
+};
+
+void emit_prelude(std::ostringstream& o) {
+  o << R"PRE(#include "tc_bodies.h"
+namespace tcgj {
+template <class TR, class RD, class WR, class CT>
+struct Acc {
+  RD& rd_;
+  WR& wr_;
+  CT& ct_;
+  long long px_, py_, pz_;
+  __device__ __forceinline__ double read(int a, int dx, int dy, int dz) const { return rd_(a, dx, dy, dz); }
+  __device__ __forceinline__ void write(int a, double v) const { wr_(a, v, 0); }
+  __device__ __forceinline__ void increment(int a, double v) const { wr_(a, v, 1); }
+  __device__ __forceinline__ void contribute(double v) const { ct_(v); }
+  __device__ __forceinline__ long long x() const { return px_; }
+  __device__ __forceinline__ long long y() const { return py_; }
+  __device__ __forceinline__ long long z() const { return pz_; }
+  __device__ __forceinline__ int nargs() const { return TR::nargs; }
+  __device__ __forceinline__ int mode(int a) const { return TR::mode(a); }
+  __device__ __forceinline__ int npts(int a) const { return TR::npts(a); }
+  __device__ __forceinline__ int pt(int a, int j, int d) const { return TR::pt(a, j, d); }
+  __device__ __forceinline__ bool reduces() const { return TR::red; }
+};
+__device__ __forceinline__ double comb(int op, double a, double b) {
+  return op == 0 ? a + b : (op == 1 ? (a < b ? a : b) : (a > b ? a : b));
+}
+__device__ __forceinline__ double ident(int op) {
+  return op == 0 ? 0.0 : (op == 1 ? __longlong_as_double(0x7ff0000000000000LL) : __longlong_as_double(0xfff0000000000000LL));
+}
+// Bit j: point j of the thread (x = cx0 + (j % BX) * SX, y = cy0 + j / BX)
+// inside [xlo, xhi) x [ylo, yhi).
+template <int P, int BX, int SX>
+__device__ __forceinline__ unsigned cmask(int cx0, int cy0, int xlo, int xhi, int ylo, int yhi) {
+  unsigned m = 0;
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const int x = cx0 + (j % BX) * SX, y = cy0 + j / BX;
+    if (x >= xlo && x < xhi && y >= ylo && y < yhi) m |= 1u << j;
+  }
+  return m;
+}
+__device__ __forceinline__ void pf_l2(const double* p, long long n) {
+  const unsigned long long a0 = reinterpret_cast<unsigned long long>(p) & ~15ULL;
+  const unsigned long long a1 = (reinterpret_cast<unsigned long long>(p + n) + 15ULL) & ~15ULL;
+  if (a1 > a0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+}
+__device__ __forceinline__ double nanv() { return __longlong_as_double(0x7ff8dead00000000LL); }
+__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(su32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(su32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+                   su32(m)), "r"(parity) : "memory");
+}
+// global -> shared bulk copy (TMA), completion in bytes on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(mbar)) : "memory");
+}
+}  // namespace tcgj
+)PRE";
+}
+
+std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, const Shape& S,
+                     const std::vector<StreamGeom>& geoms, const Range* red_mask, const std::vector<int32_t>& param_off,
+                     int nparams, StreamKernel& K) {
+  Gen g{ch, A, Sc, S, {}, {}, {}, {}};
+  std::ostringstream o;
+  const int P = g.P();
+  const int s = A.s;
+  const int U = Sc.unroll;
+  const int nd = static_cast<int>(A.dats.size());
+  const int BX = S.blk.bx;
+  const bool vec = A.dim == 3 && BX % 2 == 0;  // contiguous x pairs: 16-byte accesses
+  for (int k = 0; k < nd; ++k) {
+    const StreamGeom& G = geoms.at(static_cast<size_t>(A.dats[static_cast<size_t>(k)]));
+    int found = -1;
+    for (size_t c = 0; c < g.gcs.size(); ++c) {
+      const Gen::GC& q = g.gcs[c];
+      if (q.x0 == G.x0 && q.y0 == G.y0 && q.z0 == G.z0 && q.py == G.py && q.pz == G.pz && q.alloc == G.alloc)
+        found = static_cast<int>(c);
+    }
+    if (found < 0) {
+      g.gcs.push_back(Gen::GC{G.x0, G.y0, G.z0, G.py, G.pz, G.alloc});
+      found = static_cast<int>(g.gcs.size()) - 1;
+    }
+    g.slot_gc.push_back(found);
+  }
+  auto srow = [&](const Gen::GC& q) { return s == 1 ? q.y0 : q.z0; };
+  auto spitch = [&](const Gen::GC& q) { return s == 1 ? q.py : q.pz; };
+  emit_prelude(o);
+  o << "struct TcgArgs { const double* src[" << nd << "]; double* dst[" << nd
+    << "]; double* part; double* out; unsigned int* ticket; double p[" << std::max(1, nparams) << "]; };\n";
+  for (size_t li = 0; li < ch.loops.size(); ++li) {
+    if (!A.loops[li].needed) continue;
+    const LoopRecord& lp = ch.loops[li];
+    o << "struct Tr" << li << " {\n  static constexpr int nargs = " << lp.args.size() << ";\n";
+    o << "  static constexpr bool red = " << (lp.reduction ? "true" : "false") << ";\n";
+    o << "  static __device__ __forceinline__ int mode(int a) { switch (a) {";
+    for (size_t a = 0; a < lp.args.size(); ++a) o << " case " << a << ": return " << static_cast<int>(lp.args[a].mode) << ";";
+    o << " default: return -1; } }\n";
+    o << "  static __device__ __forceinline__ int npts(int a) { switch (a) {";
+    for (size_t a = 0; a < lp.args.size(); ++a)
+      o << " case " << a << ": return " << ch.stencil(lp.args[a].stencil).points().size() << ";";
+    o << " default: return 0; } }\n";
+    o << "  static __device__ __forceinline__ int pt(int a, int j, int d) { switch ((a * 256 + j) * 4 + d) {";
+    for (size_t a = 0; a < lp.args.size(); ++a) {
+      const auto& pts = ch.stencil(lp.args[a].stencil).points();
+      for (size_t j = 0; j < pts.size(); ++j)
+        for (int d = 0; d < 3; ++d)
+          if (pts[j][static_cast<size_t>(d)] != 0)
+            o << " case " << ((a * 256 + j) * 4 + static_cast<size_t>(d)) << ": return " << pts[j][static_cast<size_t>(d)]
+              << ";";
+    }
+    o << " default: return 0; } }\n};\n";
+  }
+  const int64_t hx0 = A.H.start(0), hx1 = A.H.end(0);
+  const int64_t hy0 = A.dim == 3 ? A.H.start(1) : 0, hy1 = A.dim == 3 ? A.H.end(1) : 1;
+  const int64_t hs0 = A.H.start(s), hs1 = A.H.end(s);
+  const int64_t esl = A.E[s][0], esh = A.E[s][1];
+  o << "#define NT " << S.nt << "\n#define P " << P << "\n#define BX " << BX << "\n#define BY " << S.blk.by
+    << "\n#define NTX " << S.ntx << "\n#define SPX " << S.spx << "\n#define SX " << g.xstep() << "\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << S.nt << ", " << S.minb
+    << ") tcg_stream(const __grid_constant__ TcgArgs A) {\n";
+  o << "  extern __shared__ __align__(128) double sm[];\n";
+  if (Sc.nbar) o << "  __shared__ __align__(8) unsigned long long bar[" << Sc.nbar << "];\n";
+  o << "  const int tid = threadIdx.x;\n  const int tx = tid % NTX, ty = tid / NTX;\n  const int cta = blockIdx.x;\n";
+  o << "  const int itx = cta % " << S.nxt << ", ity = (cta / " << S.nxt << ") % " << S.nyt << ", iseg = cta / "
+    << (S.nxt * S.nyt) << ";\n";
+  o << "  const int ox0 = " << hx0 << " + itx * " << S.wox << ", ox1 = min(ox0 + " << S.wox << ", " << hx1 << ");\n";
+  o << "  const int oy0 = " << hy0 << " + ity * " << S.woy << ", oy1 = min(oy0 + " << S.woy << ", " << hy1 << ");\n";
+  o << "  const int s0 = " << hs0 << " + static_cast<int>(static_cast<long long>(iseg) * " << (hs1 - hs0) << " / " << S.ns
+    << "), s1 = " << hs0 << " + static_cast<int>(static_cast<long long>(iseg + 1) * " << (hs1 - hs0) << " / " << S.ns
+    << ");\n";
+  // Tile origin X0 (even when rows are bulk-copied or paired: 16-byte alignment).
+  if ((A.dim == 3 && BX > 1) || Sc.ntma)
+    o << "  const int X0 = (ox0 - " << (S.exl - 1) << ") & ~1;\n";
+  else
+    o << "  const int X0 = ox0 - " << S.exl << ";\n";
+  o << "  const int cx0 = X0 + " << (A.dim == 3 ? "tx * BX" : "tid") << ";\n";
+  o << "  const int cy0 = " << (A.dim == 3 ? "oy0 - " + std::to_string(S.eyl) + " + ty * BY" : std::string("0")) << ";\n";
+  if (A.dim == 3)
+    o << "  double* const smp = sm + (ty * BY + " << S.ry << ") * SPX + tx * BX + " << S.rx << ";\n";
+  else
+    o << "  double* const smp = sm + tid + " << S.rx << ";\n";
+  o << "  (void)smp; (void)cy0; (void)oy1; (void)tx; (void)ty;\n";
+  o << "  const int tstart = s0 - " << esl << ", tend = s1 + " << (esh + Sc.lmax) << ";\n";
+  for (size_t c = 0; c < g.gcs.size(); ++c) {
+    const Gen::GC& q = g.gcs[c];
+    o << "  const long long po" << c << " = static_cast<long long>(cx0 - " << q.x0 << ")";
+    if (A.dim == 3) o << " + static_cast<long long>(cy0 - " << q.y0 << ") * " << fmt_L(q.py);
+    o << ";\n";
+  }
+  std::vector<int> loaded, tma;
+  for (size_t v = 0; v < Sc.vers.size(); ++v)
+    if (Sc.vers[v].needed && Sc.vers[v].prod < 0) (Sc.vers[v].tma ? tma : loaded).push_back(static_cast<int>(v));
+  const int rows_per = A.dim == 3 ? S.ty : 1;
+  const int nrows = static_cast<int>(tma.size()) * rows_per;  // bulk copies per step
+  const int nissue = std::min(nrows, S.nt);                     // threads issuing them
+  std::ostringstream ptrs, adv;
+  std::vector<std::string> accs;
+  std::vector<int> red_ops;
+  for (size_t li = 0; li < ch.loops.size(); ++li)
+    if (A.loops[li].needed && ch.loops[li].reduction) {
+      accs.push_back("acc" + std::to_string(accs.size()));
+      red_ops.push_back(static_cast<int>(ch.loops[li].reduction->op));
+    }
+  K.red_op = red_ops;
+  // Pointers (row of step t0, advanced by U rows per unrolled iteration).
+  for (int v : loaded) {
+    const SVer& sv = Sc.vers[static_cast<size_t>(v)];
+    const int c = g.slot_gc[static_cast<size_t>(sv.slot)];
+    const Gen::GC& q = g.gcs[static_cast<size_t>(c)];
+    ptrs << "  const double* __restrict__ lp" << v << " = A.src[" << sv.slot << "] + static_cast<long long>(tstart - "
+         << sv.lag << " - " << srow(q) << ") * " << fmt_L(spitch(q)) << " + po" << c << ";\n";
+    adv << "    lp" << v << " += " << fmt_L(spitch(q) * U) << ";\n";
+  }
+  for (size_t li = 0; li < ch.loops.size(); ++li) {
+    const SLoop& Lp = A.loops[li];
+    if (!Lp.needed) continue;
+    for (size_t a = 0; a < ch.loops[li].args.size(); ++a) {
+      const int v = Lp.vout[a];
+      if (v < 0) continue;
+      const SVer& sv = Sc.vers[static_cast<size_t>(v)];
+      if (!sv.store || !K.store[static_cast<size_t>(sv.slot)]) continue;
+      const int c = g.slot_gc[static_cast<size_t>(sv.slot)];
+      const Gen::GC& q = g.gcs[static_cast<size_t>(c)];
+      ptrs << "  double* __restrict__ sp" << v << " = A.dst[" << sv.slot << "] + static_cast<long long>(tstart - "
+           << Sc.lag[li] << " - " << srow(q) << ") * " << fmt_L(spitch(q)) << " + po" << c << ";\n";
+      adv << "    sp" << v << " += " << fmt_L(spitch(q) * U) << ";\n";
+    }
+  }
+  auto stage_store = [&](std::ostringstream& b, int v, int u, int64_t age, const std::string& indent) {
+    const int rs = g.reg_slot(v, u, age);
+    const int64_t so = g.sm_slot_off(v, u, age);
+    for (int j = 0; j < P; ++j) {
+      if (vec && g.jx(j) % 2 == 0) {
+        b << indent << "*reinterpret_cast<double2*>(&smp[" << (so + g.sm_off(j)) << "]) = make_double2(V" << v << "[" << rs
+          << "][" << j << "], V" << v << "[" << rs << "][" << (j + 1) << "]);\n";
+        ++j;
+      } else {
+        b << indent << "smp[" << (so + g.sm_off(j)) << "] = V" << v << "[" << rs << "][" << j << "];\n";
+      }
+    }
+  };
+  // ---- one step of phase u
+  auto emit_step = [&](std::ostringstream& body, int u) {
+    if (!tma.empty()) {
+      // Bulk copies of this step's input rows (read from `la` steps on).
+      body << "    if (t + " << Sc.la << " < tend && tid < " << nissue << ") {\n";
+      body << "      unsigned long long* const mb = &bar[" << (u % Sc.nbar) << "];\n      unsigned bytes = 0;\n";
+      body << "      for (int i = tid; i < " << nrows << "; i += " << nissue << ") {\n";
+      body << "        const int iv = i / " << rows_per << ", iy = i - iv * " << rows_per << ";\n";
+      body << "        (void)iy;\n";
+      for (size_t k = 0; k < tma.size(); ++k) {
+        const int v = tma[k];
+        const SVer& sv = Sc.vers[static_cast<size_t>(v)];
+        const Gen::GC& q = g.gcs[static_cast<size_t>(g.slot_gc[static_cast<size_t>(sv.slot)])];
+        const int64_t slot = (u % sv.ds);
+        body << "        if (iv == " << k << ") {\n";
+        body << "          const int r = t - " << sv.lag << ";\n";
+        if (A.dim == 3) body << "          const int yy = oy0 - " << S.eyl << " + iy;\n";
+        body << "          const int xa = max(X0, " << q.alloc.start(0) << ") & ~1, xb = (min(X0 + " << S.tx << ", "
+             << q.alloc.end(0) << ") + 1) & ~1;\n";
+        body << "          if (r >= " << q.alloc.start(s) << " && r < " << q.alloc.end(s);
+        if (A.dim == 3) body << " && yy >= " << q.alloc.start(1) << " && yy < " << q.alloc.end(1);
+        body << " && xb > xa) {\n";
+        body << "            const unsigned nb = static_cast<unsigned>(xb - xa) * 8u;\n";
+        body << "            tcgj::mbar_expect_tx(mb, nb);\n            bytes += nb;\n";
+        body << "            tcgj::bulk_g2s(sm + " << ((sv.sbase + slot) * S.sp + S.rx) << " + "
+             << (A.dim == 3 ? "(iy + " + std::to_string(S.ry) + ") * " + std::to_string(S.spx) + " + " : std::string(""))
+             << "(xa - X0), A.src[" << sv.slot << "] + static_cast<long long>(r - " << srow(q) << ") * " << fmt_L(spitch(q));
+        if (A.dim == 3) body << " + static_cast<long long>(yy - " << q.y0 << ") * " << fmt_L(q.py);
+        body << " + (xa - " << q.x0 << "), nb, mb);\n          }\n        }\n";
+      }
+      body << "      }\n      (void)bytes;\n      tcgj::mbar_arrive(mb);\n    }\n";
+    }
+    // optional L2 prefetch of input rows `prefetch` steps ahead
+    if (S.prefetch > 0 && !loaded.empty()) {
+      const int rows_per = A.dim == 3 ? S.ty : 1;
+      int idx = 0;
+      for (int v : loaded) {
+        const SVer& sv = Sc.vers[static_cast<size_t>(v)];
+        const Gen::GC& q = g.gcs[static_cast<size_t>(g.slot_gc[static_cast<size_t>(sv.slot)])];
+        body << "    if (tid >= " << idx * rows_per << " && tid < " << (idx + 1) * rows_per << ") {\n";
+        body << "      const int r = t + " << S.prefetch << " - " << sv.lag << ";\n";
+        body << "      const int yy = " << (A.dim == 3 ? "oy0 - " + std::to_string(S.eyl) : std::string("0")) << " + (tid - "
+             << idx * rows_per << ");\n";
+        body << "      const int xa = max(ox0 - " << S.exl << ", " << q.alloc.start(0) << "), xb = min(ox0 - " << S.exl << " + "
+             << S.tx << ", " << q.alloc.end(0) << ");\n";
+        body << "      if (r >= " << q.alloc.start(s) << " && r < " << q.alloc.end(s);
+        if (A.dim == 3) body << " && yy >= " << q.alloc.start(1) << " && yy < " << q.alloc.end(1);
+        body << " && xb > xa) tcgj::pf_l2(A.src[" << sv.slot << "] + static_cast<long long>(r - " << srow(q) << ") * "
+             << fmt_L(spitch(q));
+        if (A.dim == 3) body << " + static_cast<long long>(yy - " << q.y0 << ") * " << fmt_L(q.py);
+        body << " + (xa - " << q.x0 << "), xb - xa);\n    }\n";
+        ++idx;
+      }
+    }
+    // loads: the input row t - lag lands in register age 0
+    for (int v : loaded) {
+      const SVer& sv = Sc.vers[static_cast<size_t>(v)];
+      const int c = g.slot_gc[static_cast<size_t>(sv.slot)];
+      const Gen::GC& q = g.gcs[static_cast<size_t>(c)];
+      const int am = g.box_id(q.alloc);
+      const int rs = g.reg_slot(v, u, 0);
+      const int64_t ro = spitch(q) * u;
+      body << "    { // load version " << v << " (slot " << sv.slot << ")\n";
+      body << "      const int r = t - " << sv.lag << ";\n";
+      body << "      if (r >= " << q.alloc.start(s) << " && r < " << q.alloc.end(s) << ") {\n";
+      body << "        unsigned lm = m" << am << ";\n";
+      if (sv.pass_only && !sv.pass_by.empty()) {
+        body << "        unsigned inall = 0xffffffffu;\n";
+        for (int li : sv.pass_by) {
+          if (!A.loops[static_cast<size_t>(li)].needed) continue;
+          const LoopRecord& lp = ch.loops[static_cast<size_t>(li)];
+          const int rb = g.box_id(lp.range);
+          body << "        if (!(r >= " << g.s_lo(lp.range) << " && r < " << g.s_hi(lp.range) << ")) inall = 0; else inall &= m"
+               << rb << ";\n";
+        }
+        body << "        lm &= ~inall;\n";
+      }
+      for (int j = 0; j < P; ++j) {
+        const int64_t off = ro + g.g_off(q, j);
+        if (vec && g.jx(j) % 2 == 0) {
+          body << "        if (((lm >> " << j << ") & 3u) == 3u) { const double2 q = __ldg(reinterpret_cast<const double2*>(lp"
+               << v << " + " << off << ")); V" << v << "[" << rs << "][" << j << "] = q.x; V" << v << "[" << rs << "]["
+               << (j + 1) << "] = q.y; }\n";
+          body << "        else { if ((lm >> " << j << ") & 1u) V" << v << "[" << rs << "][" << j << "] = __ldg(lp" << v << " + "
+               << off << "); if ((lm >> " << (j + 1) << ") & 1u) V" << v << "[" << rs << "][" << (j + 1) << "] = __ldg(lp"
+               << v << " + " << (off + 1) << "); }\n";
+          ++j;
+        } else {
+          body << "        if ((lm >> " << j << ") & 1u) V" << v << "[" << rs << "][" << j << "] = __ldg(lp" << v << " + "
+               << off << ");\n";
+        }
+      }
+      body << "      }\n    }\n";
+    }
+    size_t racc = 0;
+    for (size_t li = 0; li < ch.loops.size(); ++li) {
+      const SLoop& Lp = A.loops[li];
+      if (!Lp.needed) continue;
+      const LoopRecord& lp = ch.loops[li];
+      const int rb = g.box_id(lp.range);
+      body << "    { // loop " << li << ": body " << lp.kernel.fn.body << ", lag " << Sc.lag[li] << "\n";
+      body << "      const int r = t - " << Sc.lag[li] << ";\n";
+      body << "      const bool rin = r >= " << g.s_lo(lp.range) << " && r < " << g.s_hi(lp.range) << ";\n";
+      body << "      const bool rown = r >= s0 && r < s1;\n      (void)rown;\n";
+      std::string redacc;
+      int redop = 0;
+      if (lp.reduction) {
+        redacc = accs[racc];
+        redop = red_ops[racc];
+        ++racc;
+        body << "      const bool rred = rown";
+        if (red_mask) body << " && r >= " << g.s_lo(*red_mask) << " && r < " << g.s_hi(*red_mask);
+        body << ";\n";
+        body << "      const unsigned mred = m_own" << (red_mask ? " & m" + std::to_string(g.box_id(*red_mask)) : "") << ";\n";
+      }
+      for (int j = 0; j < P; ++j) {
+        body << "      {\n";
+        body << "        const bool in = rin && ((m" << rb << " >> " << j << ") & 1u);\n        (void)in;\n";
+        for (size_t a = 0; a < lp.args.size(); ++a) {
+          if (Lp.vout[a] < 0) continue;
+          if (lp.args[a].mode == AccessMode::Write) {
+            body << "        double o" << a << " = 0.0;\n";
+          } else {
+            SRead r;
+            r.v = Lp.vin[a];
+            r.arg = static_cast<int>(a);
+            body << "        double o" << a << " = " << g.read_expr(li, r, j, u) << ";\n";
+          }
+        }
+        body << "        {\n          auto rd = [&](int a_, int dx_, int dy_, int dz_) -> double {\n";
+        for (size_t a = 0; a < lp.args.size(); ++a) {
+          if (!mode_reads(lp.args[a].mode)) continue;
+          if (Lp.vout[a] >= 0) {
+            body << "            if (a_ == " << a << ") return o" << a << ";\n";
+            continue;
+          }
+          body << "            if (a_ == " << a << ") {\n";
+          for (const SRead& r : Lp.reads) {
+            if (r.pass || r.arg != static_cast<int>(a)) continue;
+            body << "              if (dx_ == " << r.off[0] << " && dy_ == " << r.off[1] << " && dz_ == " << r.off[2]
+                 << ") return " << g.read_expr(li, r, j, u) << ";\n";
+          }
+          body << "            }\n";
+        }
+        body << "            return tcgj::nanv();\n          };\n";
+        body << "          auto wr = [&](int a_, double v_, int inc_) {\n";
+        for (size_t a = 0; a < lp.args.size(); ++a)
+          if (Lp.vout[a] >= 0) body << "            if (a_ == " << a << ") o" << a << " = inc_ ? o" << a << " + v_ : v_;\n";
+        body << "          };\n";
+        if (lp.reduction)
+          body << "          auto ct = [&](double v_) { " << redacc << " = (in && rred && ((mred >> " << j
+               << ") & 1u)) ? tcgj::comb(" << redop << ", " << redacc << ", v_) : " << redacc << "; };\n";
+        else
+          body << "          auto ct = [&](double) {};\n";
+        body << "          tcgj::Acc<Tr" << li << ", decltype(rd), decltype(wr), decltype(ct)> ac{rd, wr, ct, cx0 + "
+             << static_cast<int64_t>(g.jx(j)) * g.xstep();
+        if (A.dim == 2)
+          body << ", r, 0LL};\n";
+        else
+          body << ", cy0 + " << g.jy(j) << ", r};\n";
+        body << "          tcb::body_t<" << lp.kernel.fn.body << ">(ac, A.p + " << param_off[li] << ");\n        }\n";
+        for (size_t a = 0; a < lp.args.size(); ++a) {
+          if (Lp.vout[a] < 0 || Lp.prev[a] < 0) continue;
+          SRead r;
+          r.v = Lp.prev[a];
+          r.arg = static_cast<int>(a);
+          r.pass = true;
+          body << "        if (!in) o" << a << " = " << g.read_expr(li, r, j, u) << ";\n";
+        }
+        for (size_t a = 0; a < lp.args.size(); ++a)
+          if (Lp.vout[a] >= 0)
+            body << "        V" << Lp.vout[a] << "[" << g.reg_slot(Lp.vout[a], u, 0) << "][" << j << "] = o" << a << ";\n";
+        body << "      }\n";
+      }
+      for (size_t a = 0; a < lp.args.size(); ++a) {
+        const int v = Lp.vout[a];
+        if (v < 0) continue;
+        if (g.is_shared(v)) stage_store(body, v, u, 0, "      ");
+        const SVer& sv = Sc.vers[static_cast<size_t>(v)];
+        if (!sv.store || !K.store[static_cast<size_t>(sv.slot)]) continue;
+        const int c = g.slot_gc[static_cast<size_t>(sv.slot)];
+        const Gen::GC& q = g.gcs[static_cast<size_t>(c)];
+        const Range& wh = A.whull[static_cast<size_t>(sv.slot)];
+        const int wb = g.box_id(wh);
+        const int rs = g.reg_slot(v, u, 0);
+        const int64_t ro = spitch(q) * u;
+        body << "      if (rown && r >= " << g.s_lo(wh) << " && r < " << g.s_hi(wh) << ") {\n";
+        body << "        const unsigned sm_ = m_own & m" << wb << ";\n";
+        for (int j = 0; j < P; ++j) {
+          const int64_t off = ro + g.g_off(q, j);
+          if (vec && g.jx(j) % 2 == 0) {
+            body << "        if (((sm_ >> " << j << ") & 3u) == 3u) *reinterpret_cast<double2*>(sp" << v << " + " << off
+                 << ") = make_double2(V" << v << "[" << rs << "][" << j << "], V" << v << "[" << rs << "][" << (j + 1)
+                 << "]);\n";
+            body << "        else { if ((sm_ >> " << j << ") & 1u) sp" << v << "[" << off << "] = V" << v << "[" << rs << "]["
+                 << j << "]; if ((sm_ >> " << (j + 1) << ") & 1u) sp" << v << "[" << (off + 1) << "] = V" << v << "[" << rs
+                 << "][" << (j + 1) << "]; }\n";
+            ++j;
+          } else {
+            body << "        if ((sm_ >> " << j << ") & 1u) sp" << v << "[" << off << "] = V" << v << "[" << rs << "][" << j
+                 << "];\n";
+          }
+        }
+        body << "      }\n";
+      }
+      body << "    }\n";
+    }
+    // inputs enter their shared ring at age la-1 (read from age la on)
+    for (int v : loaded)
+      if (g.is_shared(v)) stage_store(body, v, u, Sc.la - 1, "    ");
+  };
+  // ---- emit: masks, rings, pointers, unrolled step loop
+  std::ostringstream steps;
+  for (int u = 0; u < U; ++u) {
+    steps << "    { // phase " << u << "\n    const int t = t0 + " << u << ";\n    if (t < tend) {\n";
+    if (!tma.empty()) {
+      int lg = 0;
+      while ((1 << lg) < Sc.nbar) ++lg;
+      steps << "    if (t - " << Sc.la << " >= tstart) tcgj::mbar_wait(&bar[" << (((u - Sc.la) % Sc.nbar + Sc.nbar) % Sc.nbar)
+            << "], static_cast<unsigned>(((t - " << Sc.la << " - tstart) >> " << lg << ") & 1));\n";
+    }
+    steps << "    __syncthreads();\n";
+    emit_step(steps, u);
+    steps << "    }\n    }\n";
+  }
+  o << "  const unsigned m_own = tcgj::cmask<P, BX, SX>(cx0, cy0, ox0, ox1, oy0, oy1);\n  (void)m_own;\n";
+  for (size_t b = 0; b < g.boxes.size(); ++b) {
+    const auto& bb = g.boxes[b];
+    o << "  const unsigned m" << b << " = tcgj::cmask<P, BX, SX>(cx0, cy0, " << bb[0] << ", " << bb[1] << ", " << bb[2]
+      << ", " << bb[3] << ");\n";
+  }
+  for (size_t v = 0; v < Sc.vers.size(); ++v) {
+    const SVer& sv = Sc.vers[v];
+    if (!sv.needed || sv.dr == 0) continue;
+    o << "  double V" << v << "[" << sv.dr << "][P];\n  #pragma unroll\n  for (int k = 0; k < " << sv.dr
+      << "; ++k)\n    #pragma unroll\n    for (int j = 0; j < P; ++j) V" << v << "[k][j] = 0.0;\n";
+  }
+  for (size_t r = 0; r < accs.size(); ++r) o << "  double " << accs[r] << " = tcgj::ident(" << red_ops[r] << ");\n";
+  o << ptrs.str();
+  if (Sc.nbar) {
+    o << "  if (tid == 0) {\n    for (int i = 0; i < " << Sc.nbar << "; ++i) tcgj::mbar_init(&bar[i], " << nissue << ");\n";
+    o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n  __syncthreads();\n";
+  }
+  o << "  for (int t0 = tstart; t0 < tend; t0 += " << U << ") {\n";
+  o << steps.str();
+  o << adv.str();
+  o << "  }\n";
+  if (!accs.empty()) {
+    const int nw = S.nt / 32;
+    o << "  __syncthreads();\n";
+    for (size_t r = 0; r < accs.size(); ++r) {
+      const int op = red_ops[r];
+      o << "  {\n    double v = " << accs[r] << ";\n";
+      o << "    #pragma unroll\n    for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
+        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
+      o << "    if ((tid & 31) == 0) sm[tid >> 5] = v;\n    __syncthreads();\n";
+      o << "    if (tid < 32) {\n      v = tid < " << nw << " ? sm[tid] : tcgj::ident(" << op << ");\n";
+      o << "      #pragma unroll\n      for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
+        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
+      o << "      if (tid == 0) A.part[" << r << " * gridDim.x + cta] = v;\n    }\n    __syncthreads();\n  }\n";
+    }
+    o << "  __shared__ unsigned int last;\n  __threadfence();\n";
+    o << "  if (tid == 0) last = atomicAdd(A.ticket, 1u) == gridDim.x - 1 ? 1u : 0u;\n  __syncthreads();\n";
+    o << "  if (last) {\n    __threadfence();\n    const int n = gridDim.x;\n";
+    for (size_t r = 0; r < accs.size(); ++r) {
+      const int op = red_ops[r];
+      o << "    {\n      const int chunk = (n + NT - 1) / NT;\n      const int a0 = tid * chunk, a1 = a0 + chunk < n ? a0 + chunk : n;\n";
+      o << "      double v = tcgj::ident(" << op << ");\n";
+      o << "      for (int i = a0; i < a1; ++i) v = tcgj::comb(" << op << ", v, __ldcg(A.part + " << r << " * n + i));\n";
+      o << "      #pragma unroll\n      for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
+        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
+      o << "      if ((tid & 31) == 0) sm[tid >> 5] = v;\n      __syncthreads();\n";
+      o << "      if (tid < 32) {\n        v = tid < " << nw << " ? sm[tid] : tcgj::ident(" << op << ");\n";
+      o << "        #pragma unroll\n        for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
+        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
+      o << "        if (tid == 0) A.out[" << r << "] = v;\n      }\n      __syncthreads();\n    }\n";
+    }
+    o << "    if (tid == 0) *A.ticket = 0u;\n  }\n";
+  }
+  o << "}\n";
+  return o.str();
+}
+
+uint64_t fnv(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+LoopChain slice_chain(const LoopChain& ch, size_t b, size_t e) {
+  LoopChain s;
+  s.dim = ch.dim;
+  s.stencils = ch.stencils;
+  s.loops.assign(ch.loops.begin() + static_cast<std::ptrdiff_t>(b), ch.loops.begin() + static_cast<std::ptrdiff_t>(e));
+  return s;
+}
+
+// Is dataset ds's state after loop `end` of `ch` overwritten, before any
+// read, by a later loop whose range covers `box`? Then a kernel ending at
+// `end` need not store it (the later kernel of the same flush recomputes it).
+bool dead_after(const LoopChain& ch, size_t end, DatasetId ds, const Range& box) {
+  for (size_t l = end; l < ch.loops.size(); ++l) {
+    const LoopRecord& lp = ch.loops[l];
+    bool reads = false, writes_w = false;
+    for (const ArgSpec& a : lp.args) {
+      if (a.dataset != ds) continue;
+      if (mode_reads(a.mode)) reads = true;
+      if (a.mode == AccessMode::Write) writes_w = true;
+    }
+    if (reads) return false;
+    if (writes_w) return lp.range.contains(box);
+  }
+  return false;
+}
+
+}  // namespace
+
+std::string StreamPlan::summary() const {
+  std::ostringstream o;
+  for (const StreamKernel& k : kernels) {
+    o << "kernel loops=[" << k.begin << "," << k.end << ") nt=" << k.nt << " bx=" << k.bx << " by=" << k.by
+      << " tile=" << k.tile[0] << "x" << k.tile[1] << " owned=" << k.owned[0] << "x" << k.owned[1] << " grid=" << k.grid[0]
+      << "x" << k.grid[1] << "x" << k.grid[2] << " ctas=" << k.nctas << " minb=" << k.minb << " smem=" << k.smem_bytes
+      << " lag=" << k.lag_max << " ring=" << k.ring_doubles << " smem_rows=" << k.smem_stages << " ext=";
+    for (int d = 0; d < k.dim; ++d) o << (d ? "," : "") << k.ext[d][0] << "/" << k.ext[d][1];
+    o << " computed=" << k.computed_points << " recorded=" << k.recorded_points << " stored=";
+    for (size_t i = 0; i < k.dats.size(); ++i)
+      if (k.store[i]) o << k.dats[i] << (k.pingpong[i] ? "p" : "i") << ";";
+    o << "\n";
+  }
+  return o.str();
+}
+
+StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeom>& geoms, const StreamDevice& dev,
+                             const StreamChoice& choice_in, const Range* red_mask) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (chain.dim < 2) throw PlanError("stream executor: 1D chains are not streamed");
+  StreamChoice choice = choice_in;
+  if (const char* e = std::getenv("TCG_STREAM_CFG")) {
+    // nt,bx,by,ntx,segments,max_loops,minb,prefetch
+    int v[8] = {0, 0, 0, 0, 0, 0, 0, -1};
+    std::sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6], &v[7]);
+    if (v[0]) choice.nt = v[0];
+    if (v[1]) choice.bx = v[1];
+    if (v[2]) choice.by = v[2];
+    if (v[3]) choice.ntx = v[3];
+    if (v[4]) choice.segments = v[4];
+    if (v[5]) choice.max_loops = v[5];
+    if (v[6]) choice.minb = v[6];
+    if (v[7] >= 0) choice.prefetch = v[7];
+  }
+  StreamPlan plan;
+  const size_t L = chain.size();
+  const size_t hmax = choice.max_loops > 0 ? static_cast<size_t>(choice.max_loops)
+                                           : static_cast<size_t>(env_int("TCG_STREAM_MAX_LOOPS", 32));
+  // Datasets whose state after loop `end` a later loop of this flush
+  // overwrites before reading: kernels ending there need not store them.
+  auto nostore_at = [&](size_t b, size_t e) {
+    std::vector<DatasetId> ns;
+    const LoopChain sub = slice_chain(chain, b, e);
+    const Analysis A = analyze(sub);
+    for (size_t k = 0; k < A.dats.size(); ++k)
+      if (A.final_ver[k] >= 0 && dead_after(chain, e, A.dats[k], A.whull[k])) ns.push_back(A.dats[k]);
+    return ns;
+  };
+  size_t begin = 0;
+  while (begin < L) {
+    // Sub-chain length: the prefix with the best estimated time per loop
+    // (fusing more loops saves HBM traffic but widens the overlapped halo).
+    size_t best_end = 0;
+    double best_rate = 1e300;
+    const size_t last = std::min(L, begin + hmax);
+    for (size_t end = (choice.max_loops > 0 ? last : begin + 1); end <= last; ++end) {
+      const LoopChain sub = slice_chain(chain, begin, end);
+      const Analysis A = analyze(sub, nostore_at(begin, end));
+      if (!A.any_out) {
+        if (best_end == 0) best_end = end;
+        continue;
+      }
+      Sched sc;
+      Shape S;
+      try {
+        S = size_kernel(A, sub, dev, choice, sc);
+      } catch (const PlanError&) {
+        if (choice.max_loops > 0 && end > begin + 1) {
+          end -= 2;  // explicit length does not fit: try one loop less
+          continue;
+        }
+        break;  // longer prefixes only need more
+      }
+      const double rate = S.est_s / static_cast<double>(end - begin);
+      if (choice.max_loops > 0) {
+        best_end = end;
+        break;
+      }
+      if (rate < best_rate) {
+        best_rate = rate;
+        best_end = end;
+      }
+    }
+    if (best_end == 0) throw PlanError("stream executor: a single loop does not fit");
+    const size_t end = best_end;
+    const LoopChain sub = slice_chain(chain, begin, end);
+    const Analysis A = analyze(sub, nostore_at(begin, end));
+    StreamKernel K;
+    K.begin = begin;
+    K.end = end;
+    K.dim = chain.dim;
+    K.dats = A.dats;
+    const size_t nd = A.dats.size();
+    K.load.assign(nd, 0);
+    K.store.assign(nd, 0);
+    K.pingpong.assign(nd, 0);
+    K.store_box.assign(nd, Range(chain.dim));
+    for (size_t k = 0; k < nd; ++k) {
+      const int iv = A.input_ver[k];
+      K.load[k] = iv >= 0 && A.vers[static_cast<size_t>(iv)].needed;
+      if (A.final_ver[k] >= 0 && A.vers[static_cast<size_t>(A.final_ver[k])].store) {
+        K.store[k] = 1;
+        K.store_box[k] = A.whull[k];
+        // In place is safe only when no CTA can read the dataset's starting
+        // state at a point some CTA overwrites: the input is read only to
+        // pass through points outside the first writer's range, and every
+        // later writer stays inside that range.
+        const bool inplace = iv < 0 || !A.vers[static_cast<size_t>(iv)].needed ||
+                             (A.vers[static_cast<size_t>(iv)].pass_only && A.all_w_in_first[k]);
+        K.pingpong[k] = inplace ? 0 : 1;
+      }
+    }
+    int np = 0;
+    for (const LoopRecord& lp : sub.loops) {
+      K.param_off.push_back(np);
+      np += static_cast<int>(lp.kernel.fn.params.size());
+    }
+    K.nparams = np;
+    if (!A.any_out) {
+      K.nt = 32;
+      K.nctas = 0;
+      plan.kernels.push_back(K);
+      begin = end;
+      continue;
+    }
+    Sched sc;
+    const Shape S = size_kernel(A, sub, dev, choice, sc);
+    K.nt = S.nt;
+    K.minb = S.minb;
+    K.bx = S.blk.bx;
+    K.by = S.blk.by;
+    K.ntx = S.ntx;
+    K.smem_bytes = static_cast<int>(S.smem_bytes);
+    K.nctas = S.nxt * S.nyt * S.ns;
+    K.tile[0] = S.tx;
+    K.tile[1] = S.ty;
+    K.owned[0] = static_cast<int>(S.wox);
+    K.owned[1] = static_cast<int>(S.woy);
+    K.grid[0] = static_cast<int>(S.nxt);
+    K.grid[1] = static_cast<int>(S.nyt);
+    K.grid[2] = static_cast<int>(S.ns);
+    for (int d = 0; d < 3; ++d)
+      for (int e = 0; e < 2; ++e) K.ext[d][e] = A.E[d][e];
+    K.lag_max = static_cast<int>(sc.lmax);
+    K.ring_doubles = sc.reg_doubles;
+    K.smem_stages = sc.smem_rows;
+    int nloops_live = 0;
+    for (size_t li = 0; li < sub.size(); ++li) {
+      K.recorded_points += sub.loops[li].range.volume();
+      nloops_live += A.loops[li].needed ? 1 : 0;
+    }
+    const int64_t hs = A.H.extent(A.s);
+    const int64_t steps_total = hs + S.ns * (A.E[A.s][0] + A.E[A.s][1] + sc.lmax);
+    K.computed_points = static_cast<int64_t>(nloops_live) * S.nxt * S.tx * S.nyt * S.ty * steps_total;
+    K.source = generate(sub, A, sc, S, geoms, red_mask, K.param_off, np, K);
+    K.hash = fnv(K.source);
+    plan.kernels.push_back(std::move(K));
+    begin = end;
+  }
+  plan.build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return plan;
+}
+
+}  // namespace tcg

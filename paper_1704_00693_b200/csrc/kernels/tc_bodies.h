@@ -222,116 +222,119 @@ TC_HD bool dispatch(int32_t body, F&& f) {
   }
 }
 
-// Dispatch one body at one point. Returns false for an unknown id.
+// One body, selected at compile time: only the matching branch is
+// instantiated (the generated streaming kernels call body_t<B> directly).
+template <int B, class A>
+TC_HD void body_t(A& a, const double* p) {
+  (void)p;
+  if constexpr (B == kGenSum) {
+    gen_sum(a, p);
+  } else if constexpr (B == kJacobiStencil) {  // proj/core/src/apps.cpp:43-57
+    a.write(1, 0.5 * a.read(0, 0, 0, 0) +
+                   0.125 * (a.read(0, 1, 0, 0) + a.read(0, -1, 0, 0) + a.read(0, 0, 1, 0) + a.read(0, 0, -1, 0)));
+  } else if constexpr (B == kJacobiCopy) {
+    a.write(1, a.read(0, 0, 0, 0));
+  } else if constexpr (B == kMhEos) {  // proj/core/src/apps.cpp:163-254 (mini-hydro)
+    a.write(2, 0.4 * a.read(0, 0, 0, 0) * a.read(1, 0, 0, 0));
+  } else if constexpr (B == kMhBcX) {
+    a.write(1, a.read(0, 1, 0, 0));
+  } else if constexpr (B == kMhBcY) {
+    a.write(1, a.read(0, 0, 1, 0));
+  } else if constexpr (B == kMhAccelX) {
+    a.increment(1, 0.01 * (a.read(0, 1, 0, 0) - a.read(0, 0, 0, 0)));
+  } else if constexpr (B == kMhAccelY) {
+    a.increment(1, 0.01 * (a.read(0, 0, 1, 0) - a.read(0, 0, 0, 0)));
+  } else if constexpr (B == kMhFluxX) {
+    a.write(2, 0.5 * (a.read(0, 0, 0, 0) * a.read(1, 0, 0, 0) + a.read(0, 1, 0, 0) * a.read(1, 1, 0, 0)));
+  } else if constexpr (B == kMhFluxY) {
+    a.write(2, 0.5 * (a.read(0, 0, 0, 0) * a.read(1, 0, 0, 0) + a.read(0, 0, 1, 0) * a.read(1, 0, 1, 0)));
+  } else if constexpr (B == kMhAdvectRho) {
+    a.increment(2, 0.01 * (a.read(0, -1, 0, 0) - a.read(0, 0, 0, 0) + a.read(1, 0, -1, 0) - a.read(1, 0, 0, 0)));
+  } else if constexpr (B == kMhAdvectE) {
+    a.increment(2, 0.005 * (a.read(0, -1, 0, 0) - a.read(0, 0, 0, 0) + a.read(1, 0, -1, 0) - a.read(1, 0, 0, 0)));
+  } else if constexpr (B == kMhSmooth) {
+    a.write(1, 0.25 * (a.read(0, 1, 0, 0) + a.read(0, -1, 0, 0) + a.read(0, 0, 1, 0) + a.read(0, 0, -1, 0)));
+  } else if constexpr (B == kMhBlend) {
+    a.write(0, 0.9 * a.read(0, 0, 0, 0) + 0.1 * a.read(1, 0, 0, 0));
+  } else if constexpr (B == kMhMonitor) {
+    a.contribute(a.read(0, 0, 0, 0));
+  } else if constexpr (B == kSmooth2D) {  // proj/tests/test_executor.cpp:29-33, test_dist.cpp:27-60
+    a.write(1, 0.5 * a.read(0, 0, 0, 0) +
+                   0.125 * (a.read(0, -1, 0, 0) + a.read(0, 1, 0, 0) + a.read(0, 0, -1, 0) + a.read(0, 0, 1, 0)));
+  } else if constexpr (B == kSmooth1D) {
+    a.write(1, 0.5 * a.read(0, 0, 0, 0) + 0.25 * (a.read(0, -1, 0, 0) + a.read(0, 1, 0, 0)));
+  } else if constexpr (B == kConsume1D) {
+    a.write(1, 0.25 * (a.read(0, -1, 0, 0) + a.read(0, 0, 0, 0) + a.read(0, 1, 0, 0)));
+  } else if constexpr (B == kCopy) {
+    a.write(1, a.read(0, 0, 0, 0));
+  } else if constexpr (B == kSumRead) {
+    a.contribute(a.read(0, 0, 0, 0));
+  } else if constexpr (B == kIota) {
+    a.write(0, static_cast<double>(a.x()));
+  } else if constexpr (B == kNbrSum) {
+    a.write(1, a.read(0, -1, 0, 0) + a.read(0, 1, 0, 0));
+  } else if constexpr (B == kHeatLap) {  // c1 heat: v = u + 0.1 * (E + W + N + S - 4u)
+    const double c = a.read(0, 0, 0, 0);
+    const double lap =
+        (((a.read(0, 1, 0, 0) + a.read(0, -1, 0, 0)) + a.read(0, 0, 1, 0)) + a.read(0, 0, -1, 0)) - 4.0 * c;
+    a.write(1, c + 0.1 * lap);
+  } else if constexpr (B == kHeatCopy) {
+    a.write(1, a.read(0, 0, 0, 0));
+  } else if constexpr (B == kHydroCfl) {  // c2: cell-wise CFL-like expression, min-reduced
+    // Named reads: the three loads are sequenced (rho, p, c) in every
+    // instantiation, whatever the accessor.
+    const double rho = a.read(0, 0, 0, 0);
+    const double pr = a.read(1, 0, 0, 0);
+    const double cs = a.read(2, 0, 0, 0);
+    a.contribute(0.5 / (rho + pr * cs));
+  } else if constexpr (B == kJacobi3D) {
+    // c3: b = 0.5*a + 0.5*(sum of 6 neighbours * 1/6) -- the 1/6 averaging
+    // coefficient is a constant product (no per-point IEEE division).
+    const double s = ((((a.read(0, 1, 0, 0) + a.read(0, -1, 0, 0)) + a.read(0, 0, 1, 0)) + a.read(0, 0, -1, 0)) +
+                      a.read(0, 0, 0, 1)) +
+                     a.read(0, 0, 0, -1);
+    a.write(1, 0.5 * a.read(0, 0, 0, 0) + 0.5 * (s * (1.0 / 6.0)));
+  } else if constexpr (B == kCgPUpdate) {  // c4 CG: p (RW), r (R); params [beta]
+    a.write(0, a.read(1, 0, 0, 0) + p[0] * a.read(0, 0, 0, 0));
+  } else if constexpr (B == kCgMatvec) {  // p (R star5), kx (R {0,-x}), ky (R {0,-y}), q (W)
+    const double pc = a.read(0, 0, 0, 0);
+    const double kxe = a.read(1, 0, 0, 0), kxw = a.read(1, -1, 0, 0);
+    const double kyn = a.read(2, 0, 0, 0), kys = a.read(2, 0, -1, 0);
+    const double diag = (((1.0 + kxe) + kxw) + kyn) + kys;
+    const double q = ((((diag * pc - kxe * a.read(0, 1, 0, 0)) - kxw * a.read(0, -1, 0, 0)) - kyn * a.read(0, 0, 1, 0)) -
+                      kys * a.read(0, 0, -1, 0));
+    a.write(3, q);
+    a.contribute(pc * q);
+  } else if constexpr (B == kCgXUpdate) {  // x (RW), p (R); params [alpha]
+    a.write(0, a.read(0, 0, 0, 0) + p[0] * a.read(1, 0, 0, 0));
+  } else if constexpr (B == kCgRUpdate) {  // r (RW), q (R); params [alpha]
+    const double r = a.read(0, 0, 0, 0) - p[0] * a.read(1, 0, 0, 0);
+    a.write(0, r);
+    a.contribute(r * r);
+  } else if constexpr (B == kCgDot) {
+    const double r = a.read(0, 0, 0, 0);
+    a.contribute(r * r);
+  } else if constexpr (B >= kHydroBase && B < kHydroBase + 10) {
+    hydro_loop(a, (B - kHydroBase) >> 1, ((B - kHydroBase) & 1) != 0);
+  } else {
+    static_assert(ns_body_known(B), "body id not in the registry");
+    ns_body_t<B>(a, p);
+  }
+}
+
+// Dispatch one body at one point (run-time id). Returns false for an unknown id.
 template <class A>
 TC_HD bool run_body(int32_t body, A& a, const double* p) {
   switch (body) {
-    case kGenSum: gen_sum(a, p); return true;
-    // proj/core/src/apps.cpp:43-57
-    case kJacobiStencil:
-      a.write(1, 0.5 * a.read(0, 0, 0, 0) +
-                     0.125 * (a.read(0, 1, 0, 0) + a.read(0, -1, 0, 0) + a.read(0, 0, 1, 0) +
-                              a.read(0, 0, -1, 0)));
-      return true;
-    case kJacobiCopy: a.write(1, a.read(0, 0, 0, 0)); return true;
-    // proj/core/src/apps.cpp:163-254 (mini-hydro)
-    case kMhEos: a.write(2, 0.4 * a.read(0, 0, 0, 0) * a.read(1, 0, 0, 0)); return true;
-    case kMhBcX: a.write(1, a.read(0, 1, 0, 0)); return true;
-    case kMhBcY: a.write(1, a.read(0, 0, 1, 0)); return true;
-    case kMhAccelX: a.increment(1, 0.01 * (a.read(0, 1, 0, 0) - a.read(0, 0, 0, 0))); return true;
-    case kMhAccelY: a.increment(1, 0.01 * (a.read(0, 0, 1, 0) - a.read(0, 0, 0, 0))); return true;
-    case kMhFluxX:
-      a.write(2, 0.5 * (a.read(0, 0, 0, 0) * a.read(1, 0, 0, 0) + a.read(0, 1, 0, 0) * a.read(1, 1, 0, 0)));
-      return true;
-    case kMhFluxY:
-      a.write(2, 0.5 * (a.read(0, 0, 0, 0) * a.read(1, 0, 0, 0) + a.read(0, 0, 1, 0) * a.read(1, 0, 1, 0)));
-      return true;
-    case kMhAdvectRho:
-      a.increment(2, 0.01 * (a.read(0, -1, 0, 0) - a.read(0, 0, 0, 0) + a.read(1, 0, -1, 0) -
-                             a.read(1, 0, 0, 0)));
-      return true;
-    case kMhAdvectE:
-      a.increment(2, 0.005 * (a.read(0, -1, 0, 0) - a.read(0, 0, 0, 0) + a.read(1, 0, -1, 0) -
-                              a.read(1, 0, 0, 0)));
-      return true;
-    case kMhSmooth:
-      a.write(1, 0.25 * (a.read(0, 1, 0, 0) + a.read(0, -1, 0, 0) + a.read(0, 0, 1, 0) +
-                         a.read(0, 0, -1, 0)));
-      return true;
-    case kMhBlend: a.write(0, 0.9 * a.read(0, 0, 0, 0) + 0.1 * a.read(1, 0, 0, 0)); return true;
-    case kMhMonitor: a.contribute(a.read(0, 0, 0, 0)); return true;
-    // proj/tests/test_executor.cpp:29-33, test_dist.cpp:27-60
-    case kSmooth2D:
-      a.write(1, 0.5 * a.read(0, 0, 0, 0) +
-                     0.125 * (a.read(0, -1, 0, 0) + a.read(0, 1, 0, 0) + a.read(0, 0, -1, 0) +
-                              a.read(0, 0, 1, 0)));
-      return true;
-    case kSmooth1D:
-      a.write(1, 0.5 * a.read(0, 0, 0, 0) + 0.25 * (a.read(0, -1, 0, 0) + a.read(0, 1, 0, 0)));
-      return true;
-    case kConsume1D:
-      a.write(1, 0.25 * (a.read(0, -1, 0, 0) + a.read(0, 0, 0, 0) + a.read(0, 1, 0, 0)));
-      return true;
-    case kCopy: a.write(1, a.read(0, 0, 0, 0)); return true;
-    case kSumRead: a.contribute(a.read(0, 0, 0, 0)); return true;
-    case kIota: a.write(0, static_cast<double>(a.x())); return true;
-    case kNbrSum: a.write(1, a.read(0, -1, 0, 0) + a.read(0, 1, 0, 0)); return true;
-    // c1 heat: v = u + 0.1 * (E + W + N + S - 4u)
-    case kHeatLap: {
-      const double c = a.read(0, 0, 0, 0);
-      const double lap =
-          (((a.read(0, 1, 0, 0) + a.read(0, -1, 0, 0)) + a.read(0, 0, 1, 0)) + a.read(0, 0, -1, 0)) - 4.0 * c;
-      a.write(1, c + 0.1 * lap);
-      return true;
-    }
-    case kHeatCopy: a.write(1, a.read(0, 0, 0, 0)); return true;
-    // c2: cell-wise CFL-like expression, min-reduced
-    case kHydroCfl:
-      a.contribute(0.5 / (a.read(0, 0, 0, 0) + a.read(1, 0, 0, 0) * a.read(2, 0, 0, 0)));
-      return true;
-    // c3: b = 0.5*a + 0.5*(sum of 6 neighbours * 1/6) -- the 1/6 averaging
-    // coefficient is a constant product (no per-point IEEE division).
-    case kJacobi3D: {
-      const double s = ((((a.read(0, 1, 0, 0) + a.read(0, -1, 0, 0)) + a.read(0, 0, 1, 0)) +
-                         a.read(0, 0, -1, 0)) + a.read(0, 0, 0, 1)) + a.read(0, 0, 0, -1);
-      a.write(1, 0.5 * a.read(0, 0, 0, 0) + 0.5 * (s * (1.0 / 6.0)));
-      return true;
-    }
-    // c4 CG. Args documented in DESIGN.md §configs.
-    case kCgPUpdate:  // p (RW), r (R); params [beta]
-      a.write(0, a.read(1, 0, 0, 0) + p[0] * a.read(0, 0, 0, 0));
-      return true;
-    case kCgMatvec: {  // p (R star5), kx (R {0,-x}), ky (R {0,-y}), q (W)
-      const double pc = a.read(0, 0, 0, 0);
-      const double kxe = a.read(1, 0, 0, 0), kxw = a.read(1, -1, 0, 0);
-      const double kyn = a.read(2, 0, 0, 0), kys = a.read(2, 0, -1, 0);
-      const double diag = (((1.0 + kxe) + kxw) + kyn) + kys;
-      const double q = ((((diag * pc - kxe * a.read(0, 1, 0, 0)) - kxw * a.read(0, -1, 0, 0)) -
-                         kyn * a.read(0, 0, 1, 0)) - kys * a.read(0, 0, -1, 0));
-      a.write(3, q);
-      a.contribute(pc * q);
-      return true;
-    }
-    case kCgXUpdate:  // x (RW), p (R); params [alpha]
-      a.write(0, a.read(0, 0, 0, 0) + p[0] * a.read(1, 0, 0, 0));
-      return true;
-    case kCgRUpdate: {  // r (RW), q (R); params [alpha]
-      const double r = a.read(0, 0, 0, 0) - p[0] * a.read(1, 0, 0, 0);
-      a.write(0, r);
-      a.contribute(r * r);
-      return true;
-    }
-    case kCgDot: {
-      const double r = a.read(0, 0, 0, 0);
-      a.contribute(r * r);
-      return true;
-    }
+#define TCB_RUN(B)        \
+  case B:                 \
+    body_t<B>(a, p);      \
+    return true;
+    TCB_CORE_BODIES(TCB_RUN)
+    TCB_NS_BODIES(TCB_RUN)
+#undef TCB_RUN
     default:
-      if (body >= kHydroBase && body < kHydroBase + 10) {
-        hydro_loop(a, (body - kHydroBase) >> 1, ((body - kHydroBase) & 1) != 0);
-        return true;
-      }
-      return ns_run_body(body, a, p);
+      return false;
   }
 }
 

@@ -116,21 +116,25 @@ TC_HD void ns_kinetic(A& a) {
   a.contribute(0.5 * ((mx * mx + my * my) + mz * mz) / a.read(0, 0, 0, 0));
 }
 
-TC_HD bool ns_body_known(int32_t b) { return b >= kNsPrim && b <= kNsKinetic; }
+#if defined(__CUDACC__)
+__host__ __device__ constexpr bool ns_body_known(int32_t b) { return b >= kNsPrim && b <= kNsKinetic; }
+#else
+constexpr bool ns_body_known(int32_t b) { return b >= kNsPrim && b <= kNsKinetic; }
+#endif
 
-template <class A>
-TC_HD bool ns_run_body(int32_t body, A& a, const double* p) {
-  switch (body) {
-    case kNsPrim: ns_prim(a, p); return true;
-    case kNsRhsMass: ns_rhs_mass(a, p); return true;
-    case kNsRhsMomX: ns_rhs_mom(a, p, 0); return true;
-    case kNsRhsMomY: ns_rhs_mom(a, p, 1); return true;
-    case kNsRhsMomZ: ns_rhs_mom(a, p, 2); return true;
-    case kNsRhsEnergy: ns_rhs_energy(a, p); return true;
-    case kNsUpdate: ns_update(a, p); return true;
-    case kNsKinetic: ns_kinetic(a); return true;
-    default: return false;
-  }
+#define TCB_NS_BODIES(X) \
+  X(kNsPrim) X(kNsRhsMass) X(kNsRhsMomX) X(kNsRhsMomY) X(kNsRhsMomZ) X(kNsRhsEnergy) X(kNsUpdate) X(kNsKinetic)
+
+template <int B, class A>
+TC_HD void ns_body_t(A& a, const double* p) {
+  if constexpr (B == kNsPrim) ns_prim(a, p);
+  else if constexpr (B == kNsRhsMass) ns_rhs_mass(a, p);
+  else if constexpr (B == kNsRhsMomX) ns_rhs_mom(a, p, 0);
+  else if constexpr (B == kNsRhsMomY) ns_rhs_mom(a, p, 1);
+  else if constexpr (B == kNsRhsMomZ) ns_rhs_mom(a, p, 2);
+  else if constexpr (B == kNsRhsEnergy) ns_rhs_energy(a, p);
+  else if constexpr (B == kNsUpdate) ns_update(a, p);
+  else ns_kinetic(a);
 }
 
 template <class F>

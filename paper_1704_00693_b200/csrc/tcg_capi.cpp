@@ -5,6 +5,7 @@
 #include <cstring>
 #include <sstream>
 
+#include "host/tcg_jit.hpp"
 #include "host/tcg_runtime.hpp"
 #include "kernels/tc_bodies.h"
 
@@ -37,6 +38,7 @@ tcg::ExecMode mode_of(int mode, const int64_t* ts) {
   if (mode == TCG_TILED) return tcg::ExecMode::tiled({ts[0], ts[1], ts[2]});
   if (mode == TCG_TILED_AUTO) return tcg::ExecMode::tiled_auto();
   if (mode == TCG_WINDOWED) return tcg::ExecMode::windowed({ts[0], ts[1], ts[2]});
+  if (mode == TCG_STREAM) return tcg::ExecMode::stream();
   throw tcg::InvalidArgument("unknown exec mode " + std::to_string(mode));
 }
 
@@ -211,6 +213,40 @@ int tcg_synchronize(tcg_runtime* rt) {
 
 int tcg_report_text(tcg_runtime* rt, char* buf, int64_t n, int64_t* needed) {
   return guard([&] { put_text(rt->rt->last_report().to_text(), buf, n, needed); });
+}
+
+int tcg_set_stream_choice(tcg_runtime* rt, const int32_t cfg[8]) {
+  return guard([&] {
+    tcg::StreamChoice c;
+    c.nt = cfg[0];
+    c.bx = cfg[1];
+    c.by = cfg[2];
+    c.ntx = cfg[3];
+    c.segments = cfg[4];
+    c.max_loops = cfg[5];
+    c.minb = cfg[6];
+    c.prefetch = cfg[7];
+    rt->rt->set_stream_choice(c);
+  });
+}
+
+int tcg_stream_plan_pending(tcg_runtime* rt, int what, char* buf, int64_t n, int64_t* needed) {
+  return guard([&] {
+    tcg::StreamDevice sd;  // B200: 148 SMs, 227 KB opt-in shared memory per CTA
+    const tcg::StreamPlan p = rt->rt->stream_plan_pending(sd);
+    std::string out = p.summary();
+    for (size_t i = 0; i < p.kernels.size(); ++i) {
+      const tcg::StreamKernel& k = p.kernels[i];
+      if (what & 1) {
+        std::string log;
+        const std::string cubin = k.nctas ? tcg::jit_compile_cubin(k.source, &log) : std::string();
+        out += "compiled kernel " + std::to_string(i) + " cubin_bytes=" + std::to_string(cubin.size()) + "\n";
+        if (!log.empty()) out += log + "\n";
+      }
+      if (what & 2) out += "----- source kernel " + std::to_string(i) + "\n" + k.source;
+    }
+    put_text(out, buf, n, needed);
+  });
 }
 
 int tcg_plan_pending(tcg_runtime* rt, const int64_t ts[3], char* buf, int64_t n, int64_t* needed) {

@@ -103,6 +103,8 @@ def load_library() -> ctypes.CDLL:
         "tcg_gpu_plan_pending": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I64), ctypes.c_char_p, _I64,
                                                 ctypes.POINTER(_I64)]),
         "tcg_signature_pending": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
+        "tcg_set_stream_choice": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
+        "tcg_stream_plan_pending": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_char_p, _I64, ctypes.POINTER(_I64)]),
         "tcg_set_rank_grid": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
         "tcg_periodic_fill": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I32), _I64]),
         "tcg_upload_box": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_I64)]),
@@ -255,6 +257,12 @@ class ExecMode:
     @staticmethod
     def tiled_auto():
         return ExecMode(2, (0, 0, 0))
+
+    @staticmethod
+    def stream():
+        """The fused streaming executor (one generated kernel per chain
+        signature)."""
+        return ExecMode(4, (0, 0, 0))
 
     @staticmethod
     def windowed(ts=(0, 0, 0)):
@@ -554,6 +562,20 @@ class Runtime:
         g = list(grid) + [1] * (3 - len(grid))
         ts = list(tile_sizes) + [0] * (3 - len(tile_sizes))
         return _text(self._lib.tcg_rank_plans_pending, self._h, _arr(_I32, g[:3]), _arr(_I64, ts[:3]))
+
+    def set_stream_choice(self, nt=0, bx=0, by=0, ntx=0, segments=0, max_loops=0, minb=0, prefetch=-1):
+        """Streaming executor knobs (0 / -1 = sizer): threads per CTA, points
+        per thread along x / y, threads along x (3D), stream segments, loops
+        per kernel, min CTAs per SM, L2 prefetch distance in rows."""
+        _check(self._lib.tcg_set_stream_choice(self._h, _arr(_I32, [nt, bx, by, ntx, segments, max_loops, minb,
+                                                                    prefetch])))
+
+    def stream_plan_pending(self, compile: bool = False, source: bool = False, size: int = 1 << 26) -> str:
+        """Streaming plan of the pending chain (consumed): summary lines, plus
+        the NVRTC compile log (compile=True; no GPU needed) and the generated
+        sources (source=True)."""
+        return _text(self._lib.tcg_stream_plan_pending, self._h, (1 if compile else 0) | (2 if source else 0),
+                     size=size)
 
     def gpu_plan_pending(self, mode: ExecMode, size: int = 1 << 26) -> str:
         return _text(self._lib.tcg_gpu_plan_pending, self._h, mode.kind, _arr(_I64, mode.tile_sizes), size=size)
