@@ -13,6 +13,7 @@
 #include <map>
 #include <mutex>
 #include <sstream>
+#include <tuple>
 #include <vector>
 
 #include "tcg_types.hpp"
@@ -150,6 +151,21 @@ void jit_launch(void* func, int64_t grid, int nt, int smem_bytes, void* stream, 
                             dim3(static_cast<unsigned>(nt)), params, static_cast<size_t>(smem_bytes),
                             static_cast<cudaStream_t>(stream)),
            "cudaLaunchKernel(generated chain kernel)");
+}
+
+int jit_occupancy(void* func, int nt, int smem_bytes) {
+  static std::mutex mu;
+  static std::map<std::tuple<void*, int, int>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(func, nt, smem_bytes);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  cu_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(func), nt,
+                                                         static_cast<size_t>(smem_bytes)),
+           "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  cache[key] = n;
+  return n;
 }
 
 void jit_attributes(void* func, int* regs, int* local_bytes) {

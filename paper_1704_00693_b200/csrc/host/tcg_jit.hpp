@@ -20,6 +20,9 @@ void* jit_function(const std::string& src, uint64_t hash, int smem_bytes);
 // argument block passed by value.
 void jit_launch(void* func, int64_t grid, int nt, int smem_bytes, void* stream, const void* args, size_t arg_bytes);
 
+// Resident CTAs per SM of a loaded kernel at nt threads and smem bytes.
+int jit_occupancy(void* func, int nt, int smem_bytes);
+
 // Registers and local memory of a loaded kernel (tests, reports).
 void jit_attributes(void* func, int* regs, int* local_bytes);
 

@@ -965,8 +965,11 @@ void Runtime::run_stream(const LoopChain& chain, ExecutionReport& rep, const Tar
   for (const StreamKernel& K : plan.kernels) {
     if (K.nctas == 0) continue;
     void* fn = jit_function(K.source, K.hash, K.smem_bytes);
+    const int occ = std::max(1, jit_occupancy(fn, K.nt, K.smem_bytes));
+    const int64_t ns = K.segments_for(static_cast<int64_t>(dev.info().num_sms) * occ);
+    const int64_t nctas = K.tiles * ns;
     const size_t nd = K.dats.size();
-    buf.assign(2 * nd + 3 + static_cast<size_t>(std::max(1, K.nparams)), 0);
+    buf.assign(2 * nd + 4 + static_cast<size_t>(std::max(1, K.nparams)), 0);
     for (size_t k = 0; k < nd; ++k) {
       const int f = t.dev.at(static_cast<size_t>(K.dats[k]));
       if (K.store[k] && K.pingpong[k]) dev.sync_alt(f, K.store_box[k]);
@@ -977,27 +980,28 @@ void Runtime::run_stream(const LoopChain& chain, ExecutionReport& rep, const Tar
     }
     double *part = nullptr, *out = nullptr;
     unsigned* ticket = nullptr;
-    dev.stream_red_buffers(std::max<size_t>(1, K.red_op.size() * static_cast<size_t>(K.nctas)),
+    dev.stream_red_buffers(std::max<size_t>(1, K.red_op.size() * static_cast<size_t>(nctas)),
                            std::max<size_t>(1, nred_total), &part, &out, &ticket);
     buf[2 * nd] = reinterpret_cast<uint64_t>(part);
     buf[2 * nd + 1] = reinterpret_cast<uint64_t>(out + red_base);
     buf[2 * nd + 2] = reinterpret_cast<uint64_t>(ticket);
-    double* prm = reinterpret_cast<double*>(buf.data() + 2 * nd + 3);
+    buf[2 * nd + 3] = static_cast<uint64_t>(ns);
+    double* prm = reinterpret_cast<double*>(buf.data() + 2 * nd + 4);
     size_t pi = 0;
     for (size_t l = K.begin; l < K.end; ++l)
       for (double v : chain.loops[l].kernel.fn.params) prm[pi++] = v;
-    dev.launch_stream(fn, K.nctas, K.nt, K.smem_bytes, buf.data(), buf.size() * sizeof(uint64_t));
+    dev.launch_stream(fn, nctas, K.nt, K.smem_bytes, buf.data(), buf.size() * sizeof(uint64_t));
     for (size_t k = 0; k < nd; ++k)
       if (K.store[k] && K.pingpong[k]) dev.commit_alt(t.dev.at(static_cast<size_t>(K.dats[k])), K.store_box[k]);
     red_base += K.red_op.size();
-    rep.ctas += K.nctas;
-    rep.computed_points += K.computed_points;
+    rep.ctas += nctas;
+    rep.computed_points += K.computed_for(ns);
     rep.subchains += 1;
     rep.tile_sizes[0] = K.tile[0];
     if (chain.dim == 3) rep.tile_sizes[1] = K.tile[1];
     rep.cta_grid[0] = K.grid[0];
     rep.cta_grid[1] = K.grid[1];
-    rep.cta_grid[2] = K.grid[2];
+    rep.cta_grid[2] = static_cast<int>(ns);
   }
   rep.tiles_executed += rep.ctas;
   if (nred_total > 0) {

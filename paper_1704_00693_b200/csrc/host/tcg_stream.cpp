@@ -31,6 +31,7 @@ struct SVer {
   int ds = 0;        // shared-memory ring depth (0: none)
   int64_t sbase = 0; // shared-memory ring offset (rows)
   bool tma = false;  // input rows arrive by bulk copy into the shared ring
+  int lead = 1;      // input: steps between its load and the first read
 };
 
 struct SRead {
@@ -64,6 +65,15 @@ struct Analysis {
 };
 
 Range hull_or(const Range& a, bool a_set, const Range& b) { return a_set ? a.hull(b) : b; }
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+double env_dbl(const char* name, double dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atof(e) : dflt;
+}
 
 Analysis analyze(const LoopChain& ch, const std::vector<DatasetId>& nostore = {}) {
   Analysis A;
@@ -306,8 +316,9 @@ Sched schedule(const Analysis& A, const Block& B, int la) {
   for (size_t vi = 0; vi < S.vers.size(); ++vi) {
     SVer& v = S.vers[vi];
     if (v.prod >= 0 || !v.needed) continue;
-    v.tma = !v.pass_only;
-    const int lead = v.tma ? la : 1;
+    v.tma = !v.pass_only && env_int("TCG_STREAM_TMA", 0) != 0;
+    const int lead = v.tma ? la : env_int("TCG_STREAM_REG_LEAD", A.dim == 2 ? 2 : 1);
+    v.lead = lead;
     int64_t lag = int64_t{1} << 40;
     for (size_t li = 0; li < A.loops.size(); ++li) {
       if (!A.loops[li].needed) continue;
@@ -358,27 +369,53 @@ Sched schedule(const Analysis& A, const Block& B, int la) {
         }
     }
   }
-  // Ring depths padded to powers of two; the step loop is unrolled by the
-  // largest, so every ring slot is a compile-time index in every phase.
+  // The step loop is unrolled by a common multiple U of every ring depth, so
+  // every ring slot is a compile-time index in every phase: the least common
+  // multiple when it is small, else depths padded to powers of two.
   S.la = la;
-  S.unroll = 1;
   S.ntma = 0;
   for (SVer& v : S.vers) {
     if (!v.needed) continue;
+    // A register-loaded shared input is staged into its ring at age lead-1.
+    if (v.prod < 0 && !v.tma && v.ds > 0) v.dr = std::max(v.dr, v.lead);
     if (v.tma) {
       v.dr = 0;
       v.ds = std::max(v.ds, la + 1);
       ++S.ntma;
     }
-    v.dr = v.dr ? pow2ceil(v.dr) : 0;
-    if (v.ds > 0) v.ds = pow2ceil(v.ds);
-    S.unroll = std::max({S.unroll, v.dr, v.ds});
   }
-  if (S.ntma) {
-    S.nbar = pow2ceil(la + 1);
-    S.unroll = std::max(S.unroll, S.nbar);
-    S.rx = std::max(S.rx, 2);  // even-rounded copy ends overrun the tile by one
+  S.nbar = S.ntma ? la + 1 : 0;
+  auto lcm = [](int64_t a, int64_t b) {
+    int64_t x = a, y = b;
+    while (y) {
+      const int64_t t = x % y;
+      x = y;
+      y = t;
+    }
+    return a / x * b;
+  };
+  int64_t L = std::max(1, S.nbar);
+  for (const SVer& v : S.vers)
+    if (v.needed) {
+      if (v.dr > 0) L = lcm(L, v.dr);
+      if (v.ds > 0) L = lcm(L, v.ds);
+    }
+  if (L <= env_int("TCG_STREAM_LCM_UNROLL", 8)) {
+    S.unroll = static_cast<int>(L);
+  } else {
+    S.unroll = 1;
+    for (SVer& v : S.vers) {
+      if (!v.needed) continue;
+      v.dr = v.dr ? pow2ceil(v.dr) : 0;
+      if (v.ds > 0) v.ds = pow2ceil(v.ds);
+      S.unroll = std::max({S.unroll, v.dr, v.ds});
+    }
+    if (S.nbar) {
+      S.nbar = pow2ceil(S.nbar);
+      S.unroll = std::max(S.unroll, S.nbar);
+    }
   }
+  if (S.ntma) S.rx = std::max(S.rx, 2);  // even-rounded copy ends overrun the tile by one
   S.reg_doubles = 0;
   S.smem_rows = 0;
   int64_t off = 0;
@@ -410,14 +447,6 @@ struct Shape {
   double est_s = 0;  // estimated kernel seconds (sub-chain split)
 };
 
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e && *e ? std::atoi(e) : dflt;
-}
-double env_dbl(const char* name, double dflt) {
-  const char* e = std::getenv(name);
-  return e && *e ? std::atof(e) : dflt;
-}
 
 int est_regs(const Sched& sc, int P, int nloops) { return 2 * P * sc.reg_doubles + 6 * P + 44 + nloops / 4; }
 
@@ -426,11 +455,14 @@ int est_regs(const Sched& sc, int P, int nloops) { return 2 * P * sc.reg_doubles
 // when nothing fits.
 Shape size_kernel(const Analysis& A, const LoopChain& ch, const StreamDevice& dev, const StreamChoice& c, Sched& sc) {
   const int64_t hx = A.H.extent(0), hy = A.dim == 3 ? A.H.extent(1) : 1, hs = A.H.extent(A.s);
-  const std::vector<int> nts = c.nt ? std::vector<int>{c.nt} : std::vector<int>{64, 128, 192, 256, 384, 512};
-  const std::vector<int> bxs = c.bx ? std::vector<int>{c.bx} : std::vector<int>{1, 2, 4};
+  // Candidate shapes (measured on B200, tools/sweep_list.sh): one point per
+  // thread in 2D; 32-wide warps along x with 1-4 points along y in 3D.
+  const std::vector<int> nts = c.nt ? std::vector<int>{c.nt}
+                                    : (A.dim == 2 ? std::vector<int>{128, 192, 256, 64} : std::vector<int>{512, 256});
+  const std::vector<int> bxs = c.bx ? std::vector<int>{c.bx} : std::vector<int>{1};
   const std::vector<int> bys =
-      A.dim == 2 ? std::vector<int>{1} : (c.by ? std::vector<int>{c.by} : std::vector<int>{1, 2, 4});
-  const std::vector<int> ntxs = A.dim == 2 ? std::vector<int>{0} : (c.ntx ? std::vector<int>{c.ntx} : std::vector<int>{8, 16, 32});
+      A.dim == 2 ? std::vector<int>{1} : (c.by ? std::vector<int>{c.by} : std::vector<int>{2, 1, 4});
+  const std::vector<int> ntxs = A.dim == 2 ? std::vector<int>{0} : (c.ntx ? std::vector<int>{c.ntx} : std::vector<int>{32, 16});
   int nloops = 0;
   for (const SLoop& L : A.loops) nloops += L.needed ? 1 : 0;
   const double lat_k = env_dbl("TCG_STREAM_LAT", 6.0);
@@ -438,6 +470,7 @@ Shape size_kernel(const Analysis& A, const LoopChain& ch, const StreamDevice& de
   Shape best;
   Sched best_sc;
   best.cost = 1e300;
+  bool best_good = false;
   std::map<std::pair<int, int>, Sched> scache;
   for (int bx : bxs)
     for (int by : bys) {
@@ -490,7 +523,14 @@ Shape size_kernel(const Analysis& A, const LoopChain& ch, const StreamDevice& de
           const double lat = 1.0 + lat_k / (warps * std::min(P, 4));
           S.cost = red * lat;
           S.minb = cps;
-          if (S.cost < best.cost) {
+          // Measured preference order (candidates are listed best-first):
+          // the first shape reaching the occupancy floor wins.
+          const bool good = cps * nt >= (A.dim == 2 ? 256 : 512);
+          if (good && !(best.cost < 1e300 && best_good)) {
+            best = S;
+            best_sc = S0;
+            best_good = true;
+          } else if (!best_good && S.cost < best.cost) {
             best = S;
             best_sc = S0;
           }
@@ -698,7 +738,7 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
   auto spitch = [&](const Gen::GC& q) { return s == 1 ? q.py : q.pz; };
   emit_prelude(o);
   o << "struct TcgArgs { const double* src[" << nd << "]; double* dst[" << nd
-    << "]; double* part; double* out; unsigned int* ticket; double p[" << std::max(1, nparams) << "]; };\n";
+    << "]; double* part; double* out; unsigned int* ticket; long long ns; double p[" << std::max(1, nparams) << "]; };\n";
   for (size_t li = 0; li < ch.loops.size(); ++li) {
     if (!A.loops[li].needed) continue;
     const LoopRecord& lp = ch.loops[li];
@@ -737,9 +777,10 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
     << (S.nxt * S.nyt) << ";\n";
   o << "  const int ox0 = " << hx0 << " + itx * " << S.wox << ", ox1 = min(ox0 + " << S.wox << ", " << hx1 << ");\n";
   o << "  const int oy0 = " << hy0 << " + ity * " << S.woy << ", oy1 = min(oy0 + " << S.woy << ", " << hy1 << ");\n";
-  o << "  const int s0 = " << hs0 << " + static_cast<int>(static_cast<long long>(iseg) * " << (hs1 - hs0) << " / " << S.ns
-    << "), s1 = " << hs0 << " + static_cast<int>(static_cast<long long>(iseg + 1) * " << (hs1 - hs0) << " / " << S.ns
-    << ");\n";
+  // Stream segments: A.ns, chosen at launch from the kernel's occupancy.
+  o << "  const int s0 = " << hs0 << " + static_cast<int>(static_cast<long long>(iseg) * " << (hs1 - hs0)
+    << " / A.ns), s1 = " << hs0 << " + static_cast<int>(static_cast<long long>(iseg + 1) * " << (hs1 - hs0)
+    << " / A.ns);\n";
   // Tile origin X0 (even when rows are bulk-copied or paired: 16-byte alignment).
   if ((A.dim == 3 && BX > 1) || Sc.ntma)
     o << "  const int X0 = (ox0 - " << (S.exl - 1) << ") & ~1;\n";
@@ -779,9 +820,8 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
     const SVer& sv = Sc.vers[static_cast<size_t>(v)];
     const int c = g.slot_gc[static_cast<size_t>(sv.slot)];
     const Gen::GC& q = g.gcs[static_cast<size_t>(c)];
-    ptrs << "  const double* __restrict__ lp" << v << " = A.src[" << sv.slot << "] + static_cast<long long>(tstart - "
-         << sv.lag << " - " << srow(q) << ") * " << fmt_L(spitch(q)) << " + po" << c << ";\n";
-    adv << "    lp" << v << " += " << fmt_L(spitch(q) * U) << ";\n";
+    (void)q;
+    (void)c;
   }
   for (size_t li = 0; li < ch.loops.size(); ++li) {
     const SLoop& Lp = A.loops[li];
@@ -793,9 +833,8 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
       if (!sv.store || !K.store[static_cast<size_t>(sv.slot)]) continue;
       const int c = g.slot_gc[static_cast<size_t>(sv.slot)];
       const Gen::GC& q = g.gcs[static_cast<size_t>(c)];
-      ptrs << "  double* __restrict__ sp" << v << " = A.dst[" << sv.slot << "] + static_cast<long long>(tstart - "
-           << Sc.lag[li] << " - " << srow(q) << ") * " << fmt_L(spitch(q)) << " + po" << c << ";\n";
-      adv << "    sp" << v << " += " << fmt_L(spitch(q) * U) << ";\n";
+      (void)q;
+      (void)c;
     }
   }
   auto stage_store = [&](std::ostringstream& b, int v, int u, int64_t age, const std::string& indent) {
@@ -875,6 +914,8 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
       const int64_t ro = spitch(q) * u;
       body << "    { // load version " << v << " (slot " << sv.slot << ")\n";
       body << "      const int r = t - " << sv.lag << ";\n";
+      body << "      const double* __restrict__ lp" << v << " = A.src[" << sv.slot << "] + (rb" << c << " - "
+           << fmt_L(spitch(q) * sv.lag) << ");\n";
       body << "      if (r >= " << q.alloc.start(s) << " && r < " << q.alloc.end(s) << ") {\n";
       body << "        unsigned lm = m" << am << ";\n";
       if (sv.pass_only && !sv.pass_by.empty()) {
@@ -926,9 +967,15 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
         body << ";\n";
         body << "      const unsigned mred = m_own" << (red_mask ? " & m" + std::to_string(g.box_id(*red_mask)) : "") << ";\n";
       }
+      bool has_pass = false;
+      for (size_t a = 0; a < lp.args.size(); ++a) has_pass = has_pass || (Lp.vout[a] >= 0 && Lp.prev[a] >= 0);
+      auto emit_points = [&](bool fast) {
       for (int j = 0; j < P; ++j) {
         body << "      {\n";
-        body << "        const bool in = rin && ((m" << rb << " >> " << j << ") & 1u);\n        (void)in;\n";
+        if (fast)
+          body << "        const bool in = true;\n        (void)in;\n";
+        else
+          body << "        const bool in = rin && ((m" << rb << " >> " << j << ") & 1u);\n        (void)in;\n";
         for (size_t a = 0; a < lp.args.size(); ++a) {
           if (Lp.vout[a] < 0) continue;
           if (lp.args[a].mode == AccessMode::Write) {
@@ -940,6 +987,31 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
             body << "        double o" << a << " = " << g.read_expr(li, r, j, u) << ";\n";
           }
         }
+        if (lp.kernel.fn.body == 1 /* tcb::kGenSum */) {
+          // gen_sum (tc_bodies.h) expanded here, same operations in the same
+          // order: s = 0; s += every Read-arg stencil point in declaration
+          // order; out = s * p[0] + 1/16; write / blend / increment the last
+          // argument; contribute(out).
+          body << "        {\n          double s_ = 0;\n";
+          for (size_t a = 0; a < lp.args.size(); ++a) {
+            if (lp.args[a].mode != AccessMode::Read) continue;
+            for (const SRead& r : Lp.reads)
+              if (!r.pass && r.arg == static_cast<int>(a)) body << "          s_ += " << g.read_expr(li, r, j, u) << ";\n";
+          }
+          body << "          const double out_ = s_ * A.p[" << param_off[li] << "] + 0.0625;\n";
+          const size_t wi = lp.args.size() - 1;
+          const AccessMode wm = lp.args[wi].mode;
+          if (wm == AccessMode::Write)
+            body << "          o" << wi << " = out_;\n";
+          else if (wm == AccessMode::ReadWrite)
+            body << "          o" << wi << " = 0.5 * o" << wi << " + 0.5 * out_;\n";
+          else
+            body << "          o" << wi << " = o" << wi << " + 0.25 * out_;\n";
+          if (lp.reduction)
+            body << "          " << redacc << " = (in && rred && ((mred >> " << j << ") & 1u)) ? tcgj::comb(" << redop << ", "
+                 << redacc << ", out_) : " << redacc << ";\n";
+          body << "        }\n";
+        } else {
         body << "        {\n          auto rd = [&](int a_, int dx_, int dy_, int dz_) -> double {\n";
         for (size_t a = 0; a < lp.args.size(); ++a) {
           if (!mode_reads(lp.args[a].mode)) continue;
@@ -972,22 +1044,35 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
         else
           body << ", cy0 + " << g.jy(j) << ", r};\n";
         body << "          tcb::body_t<" << lp.kernel.fn.body << ">(ac, A.p + " << param_off[li] << ");\n        }\n";
+        }
         for (size_t a = 0; a < lp.args.size(); ++a) {
           if (Lp.vout[a] < 0 || Lp.prev[a] < 0) continue;
           SRead r;
           r.v = Lp.prev[a];
           r.arg = static_cast<int>(a);
           r.pass = true;
-          body << "        if (!in) o" << a << " = " << g.read_expr(li, r, j, u) << ";\n";
+          if (!fast) body << "        if (!in) o" << a << " = " << g.read_expr(li, r, j, u) << ";\n";
         }
         for (size_t a = 0; a < lp.args.size(); ++a)
-          if (Lp.vout[a] >= 0)
+          if (Lp.vout[a] >= 0 && Sc.vers[static_cast<size_t>(Lp.vout[a])].needed)
             body << "        V" << Lp.vout[a] << "[" << g.reg_slot(Lp.vout[a], u, 0) << "][" << j << "] = o" << a << ";\n";
         body << "      }\n";
       }
+      };
+      if (has_pass && A.dim == 3) {
+        // Interior fast path (3D; measured slower in 2D): every point of the thread inside the loop's
+        // range this row -- no pass-through selects.
+        body << "      if (rin && m" << rb << " == " << ((1u << P) - 1u) << "u) {\n";
+        emit_points(true);
+        body << "      } else {\n";
+        emit_points(false);
+        body << "      }\n";
+      } else {
+        emit_points(false);
+      }
       for (size_t a = 0; a < lp.args.size(); ++a) {
         const int v = Lp.vout[a];
-        if (v < 0) continue;
+        if (v < 0 || !Sc.vers[static_cast<size_t>(v)].needed) continue;
         if (g.is_shared(v)) stage_store(body, v, u, 0, "      ");
         const SVer& sv = Sc.vers[static_cast<size_t>(v)];
         if (!sv.store || !K.store[static_cast<size_t>(sv.slot)]) continue;
@@ -998,6 +1083,8 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
         const int rs = g.reg_slot(v, u, 0);
         const int64_t ro = spitch(q) * u;
         body << "      if (rown && r >= " << g.s_lo(wh) << " && r < " << g.s_hi(wh) << ") {\n";
+        body << "        double* __restrict__ sp" << v << " = A.dst[" << sv.slot << "] + (rb" << c << " - "
+             << fmt_L(spitch(q) * Sc.lag[li]) << ");\n";
         body << "        const unsigned sm_ = m_own & m" << wb << ";\n";
         for (int j = 0; j < P; ++j) {
           const int64_t off = ro + g.g_off(q, j);
@@ -1020,17 +1107,15 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
     }
     // inputs enter their shared ring at age la-1 (read from age la on)
     for (int v : loaded)
-      if (g.is_shared(v)) stage_store(body, v, u, Sc.la - 1, "    ");
+      if (g.is_shared(v)) stage_store(body, v, u, Sc.vers[static_cast<size_t>(v)].lead - 1, "    ");
   };
   // ---- emit: masks, rings, pointers, unrolled step loop
   std::ostringstream steps;
   for (int u = 0; u < U; ++u) {
     steps << "    { // phase " << u << "\n    const int t = t0 + " << u << ";\n    if (t < tend) {\n";
     if (!tma.empty()) {
-      int lg = 0;
-      while ((1 << lg) < Sc.nbar) ++lg;
       steps << "    if (t - " << Sc.la << " >= tstart) tcgj::mbar_wait(&bar[" << (((u - Sc.la) % Sc.nbar + Sc.nbar) % Sc.nbar)
-            << "], static_cast<unsigned>(((t - " << Sc.la << " - tstart) >> " << lg << ") & 1));\n";
+            << "], static_cast<unsigned>(((t - " << Sc.la << " - tstart) / " << Sc.nbar << ") & 1));\n";
     }
     steps << "    __syncthreads();\n";
     emit_step(steps, u);
@@ -1055,6 +1140,9 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
     o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n  __syncthreads();\n";
   }
   o << "  for (int t0 = tstart; t0 < tend; t0 += " << U << ") {\n";
+  for (size_t c = 0; c < g.gcs.size(); ++c)
+    o << "    const long long rb" << c << " = static_cast<long long>(t0 - " << srow(g.gcs[c]) << ") * "
+      << fmt_L(spitch(g.gcs[c])) << " + po" << c << ";\n";
   o << steps.str();
   o << adv.str();
   o << "  }\n";
@@ -1131,6 +1219,15 @@ bool dead_after(const LoopChain& ch, size_t end, DatasetId ds, const Range& box)
 
 }  // namespace
 
+int64_t StreamKernel::segments_for(int64_t slots) const {
+  if (forced_segments > 0) return std::min<int64_t>(forced_segments, stream_extent);
+  // One wave when the tiles leave room (floor: never one CTA past a wave),
+  // segments long against the pipeline warm-up.
+  int64_t ns = tiles >= slots ? 1 : slots / tiles;
+  ns = std::min<int64_t>(ns, std::max<int64_t>(1, stream_extent / min_seg));
+  return std::max<int64_t>(1, ns);
+}
+
 std::string StreamPlan::summary() const {
   std::ostringstream o;
   for (const StreamKernel& k : kernels) {
@@ -1181,16 +1278,20 @@ StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeo
   };
   size_t begin = 0;
   while (begin < L) {
-    // Sub-chain length: the prefix with the best estimated time per loop
-    // (fusing more loops saves HBM traffic but widens the overlapped halo).
+    // Sub-chain length (rule measured on B200): the longest
+    // prefix that fits the register / shared-memory budget while the
+    // overlapped tile's cross-section redundancy stays under a bound (fusing
+    // more loops saves HBM traffic but widens the halo every loop
+    // recomputes); in 3D at most TCG_STREAM_H3D loops.
     size_t best_end = 0;
-    double best_rate = 1e300;
-    const size_t last = std::min(L, begin + hmax);
-    for (size_t end = (choice.max_loops > 0 ? last : begin + 1); end <= last; ++end) {
+    const size_t cap3 = chain.dim == 3 ? static_cast<size_t>(env_int("TCG_STREAM_H3D", 3)) : L;
+    const size_t last = std::min({L, begin + hmax, begin + (choice.max_loops > 0 ? hmax : cap3)});
+    const double rmax = env_dbl(chain.dim == 2 ? "TCG_STREAM_RMAX2" : "TCG_STREAM_RMAX3", chain.dim == 2 ? 1.15 : 1.7);
+    for (size_t end = begin + 1; end <= last; ++end) {
       const LoopChain sub = slice_chain(chain, begin, end);
       const Analysis A = analyze(sub, nostore_at(begin, end));
       if (!A.any_out) {
-        if (best_end == 0) best_end = end;
+        best_end = end;
         continue;
       }
       Sched sc;
@@ -1198,21 +1299,12 @@ StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeo
       try {
         S = size_kernel(A, sub, dev, choice, sc);
       } catch (const PlanError&) {
-        if (choice.max_loops > 0 && end > begin + 1) {
-          end -= 2;  // explicit length does not fit: try one loop less
-          continue;
-        }
         break;  // longer prefixes only need more
       }
-      const double rate = S.est_s / static_cast<double>(end - begin);
-      if (choice.max_loops > 0) {
-        best_end = end;
-        break;
-      }
-      if (rate < best_rate) {
-        best_rate = rate;
-        best_end = end;
-      }
+      const double hx = static_cast<double>(A.H.extent(0)), hy = A.dim == 3 ? static_cast<double>(A.H.extent(1)) : 1.0;
+      const double red = static_cast<double>(S.nxt * S.tx) * static_cast<double>(S.nyt * S.ty) / (hx * hy);
+      if (end > begin + 1 && red > rmax && choice.max_loops == 0) break;
+      best_end = end;
     }
     if (best_end == 0) throw PlanError("stream executor: a single loop does not fit");
     const size_t end = best_end;
@@ -1282,9 +1374,14 @@ StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeo
       K.recorded_points += sub.loops[li].range.volume();
       nloops_live += A.loops[li].needed ? 1 : 0;
     }
-    const int64_t hs = A.H.extent(A.s);
-    const int64_t steps_total = hs + S.ns * (A.E[A.s][0] + A.E[A.s][1] + sc.lmax);
-    K.computed_points = static_cast<int64_t>(nloops_live) * S.nxt * S.tx * S.nyt * S.ty * steps_total;
+    K.tiles = S.nxt * S.nyt;
+    K.stream_extent = A.H.extent(A.s);
+    K.warm_rows = A.E[A.s][0] + A.E[A.s][1] + sc.lmax;
+    K.min_seg = std::max<int64_t>(8, env_int("TCG_STREAM_MIN_SEG_WARM", 4) * K.warm_rows);
+    K.tile_points = static_cast<int64_t>(S.tx) * S.ty;
+    K.live_loops = nloops_live;
+    K.forced_segments = choice.segments;
+    K.computed_points = K.computed_for(S.ns);
     K.source = generate(sub, A, sc, S, geoms, red_mask, K.param_off, np, K);
     K.hash = fnv(K.source);
     plan.kernels.push_back(std::move(K));

@@ -87,6 +87,17 @@ struct StreamKernel {
   int smem_stages = 0;       // stages staging a plane through shared memory
   int64_t computed_points = 0;  // loop-point evaluations per launch (incl. redundancy)
   int64_t recorded_points = 0;  // loop points of the recorded ranges
+  // Launch-time segment choice: CTAs = tiles x segments, segments from the
+  // compiled kernel's occupancy (whole waves), each at least min_seg rows.
+  int64_t tiles = 1;
+  int64_t stream_extent = 1;
+  int64_t min_seg = 8;
+  int64_t warm_rows = 0;          // pipeline warm-up rows per segment
+  int64_t tile_points = 1;        // computed cross-section points per CTA
+  int live_loops = 0;
+  int forced_segments = 0;        // StreamChoice::segments
+  int64_t segments_for(int64_t slots) const;
+  int64_t computed_for(int64_t ns) const { return live_loops * tiles * tile_points * (stream_extent + ns * warm_rows); }
 };
 
 struct StreamPlan {

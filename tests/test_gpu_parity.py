@@ -150,8 +150,9 @@ def test_fetch_reduction_flushes_prefix_only():
 
 
 def test_tiled_auto_switches_executor_bit_exact(oracle_lib):
-    # tiled_auto times the executors per chain signature (L2-tiled, untiled,
-    # windowed, three times each) and keeps the fastest; every flush bit-exact.
+    # tiled_auto times the executors per chain signature (untiled and the
+    # fused streaming executor, three times each) and keeps the fastest;
+    # every flush bit-exact.
     steps = 12
     want = _run_config(oracle_lib.OracleRuntime(2), configs.HydroC2, 96, steps=steps)
     rt = Runtime(2)
@@ -161,8 +162,8 @@ def test_tiled_auto_switches_executor_bit_exact(oracle_lib):
     for _ in range(steps):
         mins.append(rt.fetch_reduction(c.enqueue_step()))
         used.append(parse_report(rt.report_text())["executor"])
-    assert used[:9] == ["tiled", "untiled", "windowed"] * 3, used
-    assert len(set(used[9:])) == 1, used
+    assert used[:6] == ["untiled", "stream"] * 3, used
+    assert len(set(used[6:])) == 1, used
     got = c.outputs()
     for k in want[0]:
         assert np.array_equal(got[k], want[0][k]), k

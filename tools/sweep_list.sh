@@ -1,15 +1,3 @@
-run c2 w256_la2 "256,1,0,0,0,13,0,0"
-run c2 w128_la2 "128,1,0,0,0,13,0,0"
-run c2 w128_la3 "128,1,0,0,0,13,0,0" TCG_STREAM_LOOKAHEAD=3
-run c2 w192_la2 "192,1,0,0,0,13,0,0"
-run c2 h7_w256_la2 "256,1,0,0,0,7,0,0"
-run c2 w128b2_la2 "128,2,0,0,0,13,0,0"
-run c2 def ""
-run c3 h3_y4_la2 "256,1,4,32,0,3,0,0"
-run c3 h2_y4_la2 "256,1,4,32,0,2,0,0"
-run c3 h3_y2_la2 "256,1,2,32,0,3,0,0"
-run c3 h3_n512y2_la2 "512,1,2,32,0,3,0,0"
-run c3 h4_n512y2_la2 "512,1,2,32,0,4,0,0"
-run c3 h3_y4_la3 "256,1,4,32,0,3,0,0" TCG_STREAM_LOOKAHEAD=3
-run c1 h10_w256 "256,1,0,0,0,10,0,0"
-run c1 h10_w128 "128,1,0,0,0,10,0,0"
+for c in c2 c3 c1; do
+  run $c default ""
+done
