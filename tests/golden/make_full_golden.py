@@ -1,0 +1,98 @@
+"""Full-size parity goldens from the UNMODIFIED reference library
+(oracle/_ref/libtcref.so, built from /root/reference by oracle/Makefile).
+
+    python tests/golden/make_full_golden.py [c1 c2 c3 c4]
+
+Runs the reference Runtime at the BASELINE.json sizes with every host thread
+and records, per config, the sha256 of each final field (allocation layout,
+dim 0 fastest, fp64 bytes) and the reduction history, into
+tests/golden/ref_full.json. Per-point fields are bit-identical across the
+reference's thread counts and executors (per-point arithmetic does not
+depend on the partition); Min reductions are exact; Sum reductions (c4) depend
+on the worker fold order, so c4 records the history of this run (threads
+stated) and is compared at 1e-10 relative over the window where the reference
+agrees with itself, not by hash.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+sys.path[:0] = [str(REPO), str(REPO / "oracle"), str(REPO / "tests")]
+
+import pyoracle as po  # noqa: E402
+from paper_1704_00693_b200 import ExecMode, configs  # noqa: E402
+
+SIZES = {
+    "c1": {"n": 1024, "chains": 10},     # 100 timesteps, 10 per chain
+    "c2": {"n": 4096, "steps": 50},
+    "c3": {"n": 512, "chains": 5},       # 40 sweeps, 8 per 16-loop chain
+    "c4": {"n": 4096, "iters": 140},     # the self-consistent window of the 200-iteration run
+}
+
+
+def field_sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def run(name: str, rt, size: dict):
+    """Drives config `name` on runtime `rt` (reference or product: same calls).
+    Returns (fields dict, reduction history list)."""
+    if name == "c1":
+        c = configs.HeatC1(rt, size["n"])
+        for _ in range(size["chains"]):
+            c.enqueue_chain()
+            rt.flush()
+        return c.outputs(), []
+    if name == "c2":
+        c = configs.HydroC2(rt, size["n"])
+        mins = [rt.fetch_reduction(c.enqueue_step()) for _ in range(size["steps"])]
+        return c.outputs(), mins
+    if name == "c3":
+        c = configs.Jacobi3DC3(rt, size["n"])
+        for _ in range(size["chains"]):
+            c.enqueue_chain()
+            rt.flush()
+        return c.outputs(), []
+    if name == "c4":
+        c = configs.CgC4(rt, size["n"])
+        c.start()
+        for _ in range(size["iters"]):
+            c.iterate()
+        return c.outputs(), list(c.history)
+    raise ValueError(name)
+
+
+def main(argv):
+    names = argv or list(SIZES)
+    out_path = HERE / "ref_full.json"
+    out = json.loads(out_path.read_text()) if out_path.exists() else {}
+    threads = os.cpu_count() or 1
+    for name in names:
+        size = SIZES[name]
+        t0 = time.time()
+        rt = po.RefRuntime(3 if name == "c3" else 2, threads=threads)
+        rt.set_default_mode(ExecMode.untiled())
+        fields, hist = run(name, rt, size)
+        out[name] = {
+            "size": size,
+            "threads": threads,
+            "fields": {k: field_sha(v) for k, v in fields.items()},
+            "shapes": {k: list(v.shape) for k, v in fields.items()},
+            "history": [float(x).hex() for x in hist],
+        }
+        print(f"{name}: {time.time() - t0:.1f} s, fields {list(fields)}; history {len(hist)}", flush=True)
+        del rt, fields
+        out_path.write_text(json.dumps(out, indent=1, sort_keys=True) + "\n")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
