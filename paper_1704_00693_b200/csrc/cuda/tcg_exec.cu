@@ -601,8 +601,7 @@ DeviceExec::DeviceExec() {
   cudaStream_t st;
   TCG_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   stream_ = st;
-  TCG_CK(cudaMalloc(&red_dev_, sizeof(double) * 64));
-  TCG_CK(cudaMallocHost(&red_host_, sizeof(double) * 64));
+  ensure_red(64);
 }
 
 DeviceExec::~DeviceExec() {
@@ -920,6 +919,7 @@ void DeviceExec::download_async(int f, double* host) {
 // Chain reductions to the host through a pinned buffer (a pageable
 // destination would take the driver's staged copy path on every flush).
 void DeviceExec::read_reductions(double* out, int n) {
+  if (static_cast<size_t>(n) > red_n_) throw CudaError("read_reductions: more results than the reduction buffer holds");
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   TCG_CK(cudaMemcpyAsync(red_host_, red_dev_, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, st));
   TCG_CK(cudaStreamSynchronize(st));
@@ -994,6 +994,22 @@ void* DeviceExec::ensure_scratch(size_t bytes) {
   return scratch_;
 }
 
+// Chain reduction results (device) and their pinned host mirror: one double
+// per reducing loop of a chain, grown to the chain's count (a flush may hold
+// any number of reducing loops, runtime.cpp:94-151).
+void DeviceExec::ensure_red(size_t n) {
+  if (n <= red_n_) return;
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  TCG_CK(cudaStreamSynchronize(st));
+  if (red_dev_) TCG_CK(cudaFree(red_dev_));
+  if (red_host_) TCG_CK(cudaFreeHost(red_host_));
+  red_dev_ = nullptr;
+  red_host_ = nullptr;
+  red_n_ = std::max<size_t>({n, red_n_ * 2, 64});
+  TCG_CK(cudaMalloc(&red_dev_, sizeof(double) * red_n_));
+  TCG_CK(cudaMallocHost(&red_host_, sizeof(double) * red_n_));
+}
+
 double* DeviceExec::ensure_partials(size_t n) {
   if (n > partials_n_) {
     if (partials_) {
@@ -1058,6 +1074,7 @@ void DeviceExec::drop_graphs() {
 }
 
 void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
+  ensure_red(static_cast<size_t>(ch.nred));
   mark_chain_writes(ch);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   void* scratch = ensure_scratch(chain_bytes(ch));

@@ -153,6 +153,7 @@ class DeviceExec {
   double* partials_ = nullptr;
   size_t partials_n_ = 0;
   double* red_dev_ = nullptr;
+  size_t red_n_ = 0;  // doubles in red_dev_ / red_host_
   double* st_part_ = nullptr;
   size_t st_part_n_ = 0;
   double* st_out_ = nullptr;
@@ -186,6 +187,7 @@ class DeviceExec {
   void* take_event();
   void* ensure_scratch(size_t bytes);
   double* ensure_partials(size_t n);
+  void ensure_red(size_t n);
   PlanBufs* plan_bufs(const GpuTiledPlan& gp, uint64_t key);
 };
 

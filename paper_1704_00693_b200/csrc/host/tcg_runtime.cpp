@@ -29,6 +29,59 @@ int64_t chain_points(const LoopChain& c) {
   return n;
 }
 
+// Host-side probe of a registered body against a loop's declared arguments:
+// the body runs once on this accessor, which applies KernelCtx's checks
+// (kernel_ctx.hpp:58-89: argument index, access mode, offset in the declared
+// stencil, contribute() needs a reduction) and records the first violation.
+// The device accessors carry no checks in the default library, so a
+// mismatched declaration is refused here, at enqueue time.
+struct ProbeAcc {
+  const std::vector<ArgSpec>& args;
+  const std::vector<Stencil>& stencils;
+  bool red;
+  mutable std::string err;
+  void fail(int a, int dx, int dy, int dz, const char* why) const {
+    if (!err.empty()) return;
+    err = "arg " + std::to_string(a) + " offset (" + std::to_string(dx) + "," + std::to_string(dy) + "," +
+          std::to_string(dz) + "): " + why;
+  }
+  bool arg_ok(int a) const {
+    if (a >= 0 && static_cast<size_t>(a) < args.size()) return true;
+    fail(a, 0, 0, 0, "argument index beyond the declared arguments");
+    return false;
+  }
+  double read(int a, int dx, int dy, int dz) const {
+    if (!arg_ok(a)) return 1.0;
+    const ArgSpec& s = args[static_cast<size_t>(a)];
+    if (!mode_reads(s.mode)) fail(a, dx, dy, dz, "read through write-only arg");
+    else if (!stencils[static_cast<size_t>(s.stencil)].has_offset(dx, dy, dz)) fail(a, dx, dy, dz, "offset not in declared stencil");
+    return 1.0;
+  }
+  void write(int a, double) const {
+    if (arg_ok(a) && !mode_writes(args[static_cast<size_t>(a)].mode)) fail(a, 0, 0, 0, "write through read-only arg");
+  }
+  void increment(int a, double) const {
+    if (!arg_ok(a)) return;
+    const AccessMode m = args[static_cast<size_t>(a)].mode;
+    if (!mode_writes(m) || !mode_reads(m)) fail(a, 0, 0, 0, "increment needs a readwrite/increment arg");
+  }
+  void contribute(double) const {
+    if (!red && err.empty()) err = "contribute() without a declared reduction";
+  }
+  long long x() const { return 0; }
+  long long y() const { return 0; }
+  long long z() const { return 0; }
+  int nargs() const { return static_cast<int>(args.size()); }
+  int mode(int a) const { return arg_ok(a) ? static_cast<int>(args[static_cast<size_t>(a)].mode) : 0; }
+  int npts(int a) const {
+    return arg_ok(a) ? static_cast<int>(stencils[static_cast<size_t>(args[static_cast<size_t>(a)].stencil)].points().size()) : 0;
+  }
+  int pt(int a, int j, int d) const {
+    return static_cast<int>(stencils[static_cast<size_t>(args[static_cast<size_t>(a)].stencil)].points()[static_cast<size_t>(j)][static_cast<size_t>(d)]);
+  }
+  bool reduces() const { return red; }
+};
+
 LoopChain slice(const LoopChain& c, size_t a, size_t b) {
   LoopChain s;
   s.dim = c.dim;
@@ -217,6 +270,28 @@ ReductionHandle Runtime::par_loop(KernelHandle kernel, const Range& range, std::
                               " at offset (" + std::to_string(off[0]) + "," + std::to_string(off[1]) + "," +
                               std::to_string(off[2]) +
                               ") while writing it over an overlapping range; this races under per-point parallelism");
+    }
+  }
+  // Body signature against the declaration (once per distinct declaration).
+  {
+    uint64_t key = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) { key = (key ^ v) * 1099511628211ull; };
+    mix(static_cast<uint64_t>(kernel.fn.body));
+    mix(args.size());
+    mix(reduction ? 1 : 0);
+    mix(kernel.fn.params.size());
+    for (const ArgSpec& a : args) mix((static_cast<uint64_t>(a.stencil) << 8) | static_cast<uint64_t>(a.mode));
+    mix(stencils_.size());
+    if (!body_sig_ok_.count(key)) {
+      if (args.empty()) throw InvalidArgument("par_loop: kernel " + kernel.name + " declares no arguments");
+      ProbeAcc probe{args, stencils_, reduction.has_value(), {}};
+      std::vector<double> prm(kernel.fn.params.begin(), kernel.fn.params.end());
+      prm.resize(std::max<size_t>(prm.size(), 16), 1.0);
+      tcb::run_body(kernel.fn.body, probe, prm.data());
+      if (!probe.err.empty())
+        throw AccessError("par_loop: kernel " + kernel.name + " (body " + std::to_string(kernel.fn.body) +
+                          ") does not match its declared arguments: " + probe.err);
+      body_sig_ok_.insert(key);
     }
   }
   LoopRecord rec;

@@ -12,6 +12,7 @@
 #pragma once
 #include <map>
 #include <memory>
+#include <unordered_set>
 
 #include "tcg_comm.hpp"
 #include "tcg_dist.hpp"
@@ -223,6 +224,7 @@ class Runtime {
   int64_t max_reach_ = 0;
   std::vector<FieldRec> fields_;
   std::vector<LoopRecord> pending_;
+  std::unordered_set<uint64_t> body_sig_ok_;  // (body, declaration) pairs the probe accepted
   ExecMode default_mode_;
   std::vector<Slot> slots_;
   PlanCache plan_cache_;

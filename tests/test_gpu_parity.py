@@ -203,3 +203,24 @@ def test_ns_c5_matches_oracle(oracle_lib, mode):
         assert np.array_equal(fg[k], fo[k]), k
     for a, b in zip(kg, ko):
         assert abs(a - b) <= 1e-12 * abs(b)
+
+
+@pytest.mark.parametrize("mode", [ExecMode.untiled(), ExecMode.tiled_auto(), ExecMode.stream()],
+                         ids=["untiled", "auto", "stream"])
+def test_hundred_reducing_loops_in_one_flush(mode):
+    # A flush may hold any number of reducing loops (runtime.cpp:94-151): the
+    # device / pinned result buffers grow with the chain.
+    from paper_1704_00693_b200 import ArgSpec, AccessMode, KernelHandle, Range, ReduceOp, kernels
+    rt = Runtime(2)
+    ident = rt.declare_stencil("id", [(0, 0)])
+    dom = Range.d2(0, 24, 0, 20)
+    f0 = rt.declare_field("f0", dom)
+    rt.par_loop(KernelHandle(0, "iota", kernels.IOTA), dom, [ArgSpec(f0, ident, AccessMode.Write)])
+    handles, want = [], []
+    for i in range(100):
+        n = 1 + i % 24
+        handles.append(rt.par_loop(KernelHandle(1 + i, "sum", kernels.SUM_READ), Range.d2(0, n, 0, 20),
+                                   [ArgSpec(f0, ident, AccessMode.Read)], ReduceOp.Sum))
+        want.append(20.0 * n * (n - 1) / 2)
+    rt.flush(mode)
+    assert [rt.fetch_reduction(h) for h in handles] == want

@@ -223,6 +223,29 @@ def test_par_loop_validation():
         rt.fetch_reduction(42)
 
 
+def test_par_loop_checks_body_against_declaration():
+    # KernelCtx's access checks (kernel_ctx.hpp:58-97) applied at enqueue time
+    # by a host probe of the registered body: argument count, access modes,
+    # offsets inside the declared stencil, contribute() without a reduction.
+    from paper_1704_00693_b200.runtime import AccessError
+    rt = Runtime(1)
+    ident, three, f0, f1 = two_loop(rt)
+    n0 = rt.pending_loops()
+    with pytest.raises(AccessError, match="argument index"):  # COPY writes arg 1
+        rt.par_loop(KernelHandle(20, "short", kernels.COPY), Range.d1(0, 8), [ArgSpec(f0, ident, R)])
+    with pytest.raises(AccessError, match="write through read-only"):
+        rt.par_loop(KernelHandle(21, "ro", kernels.COPY), Range.d1(0, 8), [ArgSpec(f0, ident, R), ArgSpec(f1, ident, R)])
+    with pytest.raises(AccessError, match="read through write-only"):
+        rt.par_loop(KernelHandle(22, "wo", kernels.COPY), Range.d1(0, 8), [ArgSpec(f0, ident, W), ArgSpec(f1, ident, W)])
+    with pytest.raises(AccessError, match="offset not in declared stencil"):  # NBR_SUM reads x-1, x+1
+        rt.par_loop(KernelHandle(23, "off", kernels.NBR_SUM), Range.d1(0, 8), [ArgSpec(f0, ident, R), ArgSpec(f1, ident, W)])
+    with pytest.raises(AccessError, match="contribute"):
+        rt.par_loop(KernelHandle(24, "nored", kernels.SUM_READ), Range.d1(0, 8), [ArgSpec(f0, ident, R)])
+    assert rt.pending_loops() == n0
+    rt.par_loop(KernelHandle(25, "ok", kernels.NBR_SUM), Range.d1(0, 8), [ArgSpec(f0, three, R), ArgSpec(f1, ident, W)])
+    assert rt.pending_loops() == n0 + 1
+
+
 def _plan_ranges(text, dim):
     """TilingPlan::dump text (planner.cpp:234-250) -> flat ranges, T, L."""
     rows = {}
