@@ -104,14 +104,35 @@ int tcg_flush_default(tcg_runtime* rt);
 int tcg_set_default_mode(tcg_runtime* rt, int mode, const int64_t tile_sizes[3]);
 int tcg_fetch_reduction(tcg_runtime* rt, int32_t handle, double* out);
 int tcg_pending_loops(tcg_runtime* rt, int64_t* out);
+/* Step templates: the par_loop / periodic_fill calls made between
+ * tcg_record_begin and tcg_record_end are kept (they are enqueued normally
+ * too); tcg_replay issues the same calls again through par_loop, as the
+ * reference's C++ apps do every step (apps.cpp:59-130, :163-254), in one
+ * crossing of the binding. params (may be NULL) replaces the kernels' scalar
+ * parameters in call order. Returns the new reduction handles in call order. */
+int tcg_record_begin(tcg_runtime* rt);
+int tcg_record_end(tcg_runtime* rt, int32_t* id);
+int tcg_replay(tcg_runtime* rt, int32_t id, const double* params, int64_t nparams, int32_t* handles,
+               int64_t max_handles, int64_t* nhandles);
 
 int tcg_get(tcg_runtime* rt, int32_t ds, const int64_t p[3], double* out);
 int tcg_put(tcg_runtime* rt, int32_t ds, const int64_t p[3], double v);
 int tcg_fill_logical(tcg_runtime* rt, int32_t ds, double v);
-/* Periodic ghost copy (depth <= pad) of n fields, all dimensions; flushes
- * first. No reference counterpart (the reference has no periodic support);
- * c5 needs it. */
+/* Periodic ghost layers (depth <= pad) of n fields, all dimensions. No
+ * reference counterpart (the reference has no periodic neighbours,
+ * dist.cpp:135-140); c5 needs it. The call is
+ * RECORDED in the lazy queue like a loop: at flush the chain is rewritten so
+ * its inputs are wrapped once, to the chain's accumulated stencil reach, and
+ * the producing loops run over ranges extended into the ghost layers (the
+ * deep-halo scheme of dist.cpp:617-689 applied to the wrap-around neighbour).
+ * The RK step of c5 stays one chain. After such a chain only the logical box
+ * of a field is defined. tcg_set_periodic_flush(rt, 1) restores the eager
+ * form: flush, then copy the opposite side into the ghost layers. */
 int tcg_periodic_fill(tcg_runtime* rt, int n, const int32_t* ds, int64_t depth);
+int tcg_set_periodic_flush(tcg_runtime* rt, int flush_each);
+/* Host-only: the rewrite of the pending chain around its periodic marks
+ * (extended loop ranges, datasets wrapped before the chain); consumed. */
+int tcg_periodic_plan_pending(tcg_runtime* rt, char* buf, int64_t n, int64_t* needed);
 /* host: dense fp64 over the allocation range, dim 0 fastest. */
 int tcg_upload(tcg_runtime* rt, int32_t ds, const double* host);
 int tcg_download(tcg_runtime* rt, int32_t ds, double* host);

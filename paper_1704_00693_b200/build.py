@@ -34,7 +34,7 @@ NVCCFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler
 if DEBUG:
     NVCCFLAGS = NVCCFLAGS + ["-DTCG_DEBUG_PRINT"]
 
-HOST_SRCS = ["host/tcg_plan.cpp", "host/tcg_gpuplan.cpp", "host/tcg_dist.cpp", "host/tcg_stream.cpp", "host/tcg_jit.cpp",
+HOST_SRCS = ["host/tcg_plan.cpp", "host/tcg_gpuplan.cpp", "host/tcg_dist.cpp", "host/tcg_stream.cpp", "host/tcg_periodic.cpp", "host/tcg_jit.cpp",
              "host/tcg_runtime.cpp", "tcg_capi.cpp"]
 CUDA_SRCS = ["cuda/tcg_exec.cu", "cuda/tcg_tiled.cu", "cuda/tcg_l2.cu", "cuda/tcg_comm.cu", "cuda/tcg_stream_exec.cu"]
 

@@ -364,23 +364,32 @@ class CgC4:
         self.history = [math.sqrt(self.rr)]
         self.beta = 0.0
 
-    def iterate(self):
+    def enqueue_pq(self):
+        """p = r + beta p; q = A p with Sum p.q (first chain of an iteration)."""
         f, rt, dom, I = self.f, self.rt, self.dom, self.ident
         rt.par_loop(KernelHandle(K.CG_P_UPDATE, "p_update", K.CG_P_UPDATE, (self.beta,)), dom,
                     [ArgSpec(f["p"], I, RW), ArgSpec(f["r"], I, R)])
-        h = rt.par_loop(KernelHandle(K.CG_MATVEC, "matvec", K.CG_MATVEC), dom,
-                        [ArgSpec(f["p"], self.star, R), ArgSpec(f["kx"], self.west, R), ArgSpec(f["ky"], self.south, R),
-                         ArgSpec(f["q"], I, W)], ReduceOp.Sum)
-        pq = rt.fetch_reduction(h)
-        alpha = self.rr / pq
+        return rt.par_loop(KernelHandle(K.CG_MATVEC, "matvec", K.CG_MATVEC), dom,
+                           [ArgSpec(f["p"], self.star, R), ArgSpec(f["kx"], self.west, R), ArgSpec(f["ky"], self.south, R),
+                            ArgSpec(f["q"], I, W)], ReduceOp.Sum)
+
+    def enqueue_update(self, alpha):
+        """x += alpha p; r -= alpha q with Sum r.r (second chain)."""
+        f, rt, dom, I = self.f, self.rt, self.dom, self.ident
         rt.par_loop(KernelHandle(K.CG_X_UPDATE, "x_update", K.CG_X_UPDATE, (alpha,)), dom,
                     [ArgSpec(f["x"], I, RW), ArgSpec(f["p"], I, R)])
-        h = rt.par_loop(KernelHandle(K.CG_R_UPDATE, "r_update", K.CG_R_UPDATE, (alpha,)), dom,
-                        [ArgSpec(f["r"], I, RW), ArgSpec(f["q"], I, R)], ReduceOp.Sum)
-        rr_new = rt.fetch_reduction(h)
+        return rt.par_loop(KernelHandle(K.CG_R_UPDATE, "r_update", K.CG_R_UPDATE, (alpha,)), dom,
+                           [ArgSpec(f["r"], I, RW), ArgSpec(f["q"], I, R)], ReduceOp.Sum)
+
+    def finish_iteration(self, rr_new):
         self.beta = rr_new / self.rr
         self.rr = rr_new
         self.history.append(math.sqrt(max(rr_new, 0.0)))
+
+    def iterate(self):
+        pq = self.rt.fetch_reduction(self.enqueue_pq())
+        alpha = self.rr / pq
+        self.finish_iteration(self.rt.fetch_reduction(self.enqueue_update(alpha)))
 
     def cell_updates_per_iteration(self):
         return 4 * self.n * self.n
@@ -507,4 +516,12 @@ class NsC5:
         return 8 * per * self.n ** 3
 
     def outputs(self):
-        return {nm: self.rt.download(self.f[nm]) for nm in ("rho", "mx", "my", "mz", "E")}
+        """Conserved fields over the logical box (the ghost layers of a
+        periodic box are only defined right after a fill)."""
+        out = {}
+        for nm in ("rho", "mx", "my", "mz", "E"):
+            al = self.rt.alloc_range(self.f[nm])
+            a = self.rt.download(self.f[nm])
+            sl = tuple(slice(self.dom.start(d) - al.start(d), self.dom.end(d) - al.start(d)) for d in (2, 1, 0))
+            out[nm] = np.ascontiguousarray(a[sl])
+        return out

@@ -294,6 +294,14 @@ ReductionHandle Runtime::par_loop(KernelHandle kernel, const Range& range, std::
       body_sig_ok_.insert(key);
     }
   }
+  if (recording_) {
+    RecordedCall rc;
+    rc.kernel = kernel;
+    rc.range = range;
+    rc.args = args;
+    rc.reduction = reduction;
+    record_cur_.push_back(std::move(rc));
+  }
   LoopRecord rec;
   rec.loop_id = static_cast<int32_t>(pending_.size());
   rec.kernel = std::move(kernel);
@@ -309,17 +317,56 @@ ReductionHandle Runtime::par_loop(KernelHandle kernel, const Range& range, std::
   return h;
 }
 
+void Runtime::record_begin() {
+  recording_ = true;
+  record_cur_.clear();
+}
+
+int Runtime::record_end() {
+  if (!recording_) throw InvalidArgument("record_end: no recording in progress");
+  recording_ = false;
+  recorded_.push_back(std::move(record_cur_));
+  record_cur_.clear();
+  return static_cast<int>(recorded_.size()) - 1;
+}
+
+std::vector<ReductionHandle> Runtime::replay(int id, const double* params, size_t nparams) {
+  if (id < 0 || static_cast<size_t>(id) >= recorded_.size()) throw InvalidArgument("replay: unknown recording");
+  if (recording_) throw InvalidArgument("replay: a recording is in progress");
+  std::vector<ReductionHandle> out;
+  size_t pi = 0;
+  // The template is copied call by call: par_loop consumes its arguments.
+  for (size_t i = 0; i < recorded_[static_cast<size_t>(id)].size(); ++i) {
+    const RecordedCall& rc = recorded_[static_cast<size_t>(id)][i];
+    if (rc.fill) {
+      periodic_fill(rc.fill_ds, rc.fill_depth);
+      continue;
+    }
+    KernelHandle k = rc.kernel;
+    if (params) {
+      if (pi + k.fn.params.size() > nparams) throw InvalidArgument("replay: too few parameter values");
+      for (double& v : k.fn.params) v = params[pi++];
+    }
+    const ReductionHandle h = par_loop(std::move(k), rc.range, rc.args, rc.reduction);
+    if (rc.reduction) out.push_back(h);
+  }
+  if (params && pi != nparams) throw InvalidArgument("replay: too many parameter values");
+  return out;
+}
+
 LoopChain Runtime::take_pending() {
   LoopChain c;
   c.dim = dim_;
   c.loops = std::move(pending_);
   c.stencils = stencils_;
+  c.fills = std::move(fill_marks_);
   pending_.clear();
+  fill_marks_.clear();
   return c;
 }
 
 ExecutionReport Runtime::flush(const ExecMode& mode) {
-  if (pending_.empty()) {
+  if (pending_.empty() && fill_marks_.empty()) {
     last_report_ = ExecutionReport{};
     return last_report_;
   }
@@ -1113,7 +1160,10 @@ void Runtime::check_pad(const LoopChain& chain, const Target& t) const {
 }
 
 ExecutionReport Runtime::execute_chain(LoopChain chain, const ExecMode& mode) {
-  if (distributed()) return execute_distributed(std::move(chain), mode);
+  if (distributed()) {
+    if (!chain.fills.empty()) throw InvalidArgument("periodic_fill: not supported on a rank grid");
+    return execute_distributed(std::move(chain), mode);
+  }
   const auto t0 = std::chrono::steady_clock::now();
   ExecutionReport rep;
   rep.dim = chain.dim;
@@ -1122,6 +1172,37 @@ ExecutionReport Runtime::execute_chain(LoopChain chain, const ExecMode& mode) {
   ensure_fields();
   DeviceExec& dev = device();
   const int64_t l0 = dev.launches();
+  if (!chain.fills.empty()) {
+    // Periodic marks: one wrap of the chain's inputs to the accumulated
+    // depth, then the chain over extended ranges (tcg_periodic.hpp).
+    std::vector<Range> logical;
+    for (const FieldRec& f : fields_) logical.push_back(f.logical);
+    PeriodicPlan pp = apply_periodic(chain, logical);
+    std::map<std::pair<int64_t, std::vector<int64_t>>, std::vector<int>> groups;  // (depth, logical box) -> fields
+    for (const auto& [ds, depth] : pp.pre_fills) {
+      const FieldRec& f = fields_.at(static_cast<size_t>(ds));
+      if (depth > f.pad)
+        throw AccessError("periodic chain: needs " + std::to_string(depth) + " ghost layers of " + f.name +
+                          " but its pad is " + std::to_string(f.pad) + " (raise skew_allowance)");
+      for (int d = 0; d < dim_; ++d)
+        if (depth > f.logical.extent(d)) throw InvalidArgument("periodic chain: depth exceeds the extent of " + f.name);
+      std::vector<int64_t> key;
+      for (int d = 0; d < dim_; ++d) {
+        key.push_back(f.logical.start(d));
+        key.push_back(f.logical.end(d));
+      }
+      groups[{depth, key}].push_back(f.dev);
+    }
+    for (const auto& [k, devs] : groups) {
+      Range lg(dim_);
+      for (int d = 0; d < dim_; ++d) lg.set_raw(d, k.second[2 * static_cast<size_t>(d)], k.second[2 * static_cast<size_t>(d) + 1]);
+      dev.periodic_fill(devs, lg, k.first);
+      rep.halo_exchanges += 1;
+      rep.halo_messages += static_cast<int64_t>(devs.size()) * 2 * dim_;
+    }
+    rep.computed_points += pp.extended_points;
+    chain = std::move(pp.chain);
+  }
   const std::vector<double> vals = run_on(chain, mode, rep, whole_target());
   store(reduction_handles(chain), vals.data());
   rep.launches = dev.launches() - l0;
@@ -1482,9 +1563,21 @@ double Runtime::fetch_reduction(ReductionHandle h) {
     } else {
       std::vector<LoopRecord> suffix(pending_.begin() + static_cast<std::ptrdiff_t>(k) + 1, pending_.end());
       pending_.resize(k + 1);
+      // Periodic marks after the reducing loop stay queued with the suffix.
+      std::vector<PeriodicMark> later;
+      for (auto it = fill_marks_.begin(); it != fill_marks_.end();) {
+        if (it->pos > k) {
+          it->pos -= k + 1;
+          later.push_back(std::move(*it));
+          it = fill_marks_.erase(it);
+        } else {
+          ++it;
+        }
+      }
       execute_chain(take_pending(), default_mode_);
       for (size_t i = 0; i < suffix.size(); ++i) suffix[i].loop_id = static_cast<int32_t>(i);
       pending_ = std::move(suffix);
+      fill_marks_ = std::move(later);
     }
   }
   if (!slot.ready) throw PlanError("fetch_reduction: flush did not produce the value");
@@ -1643,9 +1736,29 @@ Range Runtime::local_box(DatasetId ds) {
 }
 
 void Runtime::periodic_fill(const std::vector<DatasetId>& list, int64_t depth) {
-  flush();
   if (distributed()) throw InvalidArgument("periodic_fill: not supported on a rank grid");
   if (depth < 0) throw InvalidArgument("periodic_fill: negative depth");
+  if (recording_) {
+    RecordedCall rc;
+    rc.fill = true;
+    rc.fill_ds = list;
+    rc.fill_depth = depth;
+    record_cur_.push_back(std::move(rc));
+  }
+  if (!periodic_flush_) {
+    // Recorded: the flush rewrites the chain around it (tcg_periodic.hpp).
+    for (DatasetId ds : list) {
+      if (ds < 0 || static_cast<size_t>(ds) >= fields_.size())
+        throw InvalidArgument("periodic_fill: unknown dataset id " + std::to_string(ds));
+      const FieldRec& f = fields_[static_cast<size_t>(ds)];
+      if (depth > f.pad) throw AccessError("periodic_fill: depth exceeds the pad of " + f.name);
+      for (int d = 0; d < dim_; ++d)
+        if (depth > f.logical.extent(d)) throw InvalidArgument("periodic_fill: depth exceeds the extent of " + f.name);
+    }
+    fill_marks_.push_back(PeriodicMark{pending_.size(), list, depth});
+    return;
+  }
+  flush();
   ensure_fields();
   // Group fields by logical box; one kernel per dimension per group.
   std::vector<std::pair<Range, std::vector<int>>> groups;

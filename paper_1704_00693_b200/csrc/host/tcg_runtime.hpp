@@ -18,6 +18,7 @@
 #include "tcg_dist.hpp"
 #include "tcg_exec.hpp"
 #include "tcg_gpuplan.hpp"
+#include "tcg_periodic.hpp"
 #include "tcg_plan.hpp"
 #include "tcg_stream.hpp"
 
@@ -109,6 +110,10 @@ class Runtime {
   // dimension so edges and corners wrap too. Flushes first. (The reference
   // has no periodic support; c5 needs it.)
   void periodic_fill(const std::vector<DatasetId>& ds, int64_t depth);
+  // true: periodic_fill flushes and wraps at once (the round-1 behaviour);
+  // false (default): it records a PeriodicMark in the queue and the chain is
+  // rewritten at flush (tcg_periodic.hpp) -- one wrap per chain.
+  void set_periodic_flush(bool v) { periodic_flush_ = v; }
   // Bulk host <-> device copies of a whole allocation (dense, dim 0 fastest,
   // the reference Field layout, field.cpp:22-26). Flush first.
   void upload(DatasetId ds, const double* host);
@@ -133,6 +138,17 @@ class Runtime {
   // Host-only: the distribution schedule of the pending chain (consumed; its
   // writes are recorded as if it had run). Needs a rank grid, no GPU.
   DistSchedule schedule_pending();
+
+  // Host-side step recording (the role of the reference's C++ apps,
+  // apps.cpp:59-130 / :163-254, which re-issue the same par_loop calls every
+  // step): between record_begin and record_end every par_loop / periodic_fill
+  // call is also kept as a template; replay(id) issues the same calls again
+  // through par_loop (validation, lazy queue, new reduction handles) without
+  // crossing the language binding once per loop. `params`, if given, replaces
+  // the kernels' scalar parameters in call order (nparams values).
+  void record_begin();
+  int record_end();
+  std::vector<ReductionHandle> replay(int id, const double* params = nullptr, size_t nparams = 0);
 
   size_t pending_loops() const { return pending_.size(); }
   LoopChain take_pending();
@@ -224,6 +240,20 @@ class Runtime {
   int64_t max_reach_ = 0;
   std::vector<FieldRec> fields_;
   std::vector<LoopRecord> pending_;
+  std::vector<PeriodicMark> fill_marks_;  // recorded periodic fills of the pending loops
+  struct RecordedCall {
+    bool fill = false;
+    KernelHandle kernel;
+    Range range;
+    std::vector<ArgSpec> args;
+    std::optional<ReduceOp> reduction;
+    std::vector<DatasetId> fill_ds;
+    int64_t fill_depth = 0;
+  };
+  bool recording_ = false;
+  std::vector<RecordedCall> record_cur_;
+  std::vector<std::vector<RecordedCall>> recorded_;
+  bool periodic_flush_ = false;
   std::unordered_set<uint64_t> body_sig_ok_;  // (body, declaration) pairs the probe accepted
   ExecMode default_mode_;
   std::vector<Slot> slots_;

@@ -30,8 +30,13 @@ struct SVer {
   int dr = 1;        // register ring depth (ages 0 .. dr-1)
   int ds = 0;        // shared-memory ring depth (0: none)
   int64_t sbase = 0; // shared-memory ring offset (rows)
-  bool tma = false;  // input rows arrive by bulk copy into the shared ring
+  bool tma = false;  // input rows arrive by bulk copy (TMA) into the shared ring
+  bool cpa = false;  // input points arrive by per-thread cp.async into the shared ring
+  bool xs = false;   // read across threads (through shared memory)
+  bool own_sm = false;  // the thread's own points are read from the shared ring too (no register ring)
+  bool fill = false; // asynchronous input with register reads: ring filled from shared memory at age `lead`
   int lead = 1;      // input: steps between its load and the first read
+  bool async_in() const { return tma || cpa; }
 };
 
 struct SRead {
@@ -265,6 +270,7 @@ struct Sched {
   int unroll = 1;       // step-loop unroll: every ring depth divides it
   int nbar = 0;         // mbarrier ring (0: no bulk-copied inputs)
   int ntma = 0;         // bulk-copied input versions
+  int ncpa = 0;         // cp.async input versions
 };
 
 int pow2ceil(int v) {
@@ -288,6 +294,26 @@ bool crosses(const Block& b, const SRead& r, int dim) {
   return false;
 }
 
+// Does a read of version v at `age` go through shared memory? Cross-thread
+// reads always do. Reads inside the thread's block come from its register
+// ring -- except, in the strided 2D layout, those of versions that are staged
+// in shared memory anyway (own_smem), which saves the ring. Asynchronously
+// loaded inputs land in shared memory first; their register ring (if any
+// in-block read needs one) is filled from there at age `lead`.
+bool read_via_smem(const SVer& v, bool in_blk, int64_t age) {
+  if (!in_blk) return true;
+  if (v.async_in()) return v.xs && v.own_sm;
+  return v.xs && v.own_sm && age >= 1;
+}
+
+// Input transport (TCG_STREAM_INPUT): 0 = register loads `lead` steps ahead,
+// 1 = TMA row copies, 2 = per-thread cp.async; 1 and 2 land in a shared ring
+// `la` steps ahead of the first read.
+int input_mode(int dim) {
+  if (env_int("TCG_STREAM_TMA", 0) != 0) return 1;
+  return env_int(dim == 2 ? "TCG_STREAM_INPUT2" : "TCG_STREAM_INPUT3", env_int("TCG_STREAM_INPUT", 2));
+}
+
 Sched schedule(const Analysis& A, const Block& B, int la) {
   Sched S;
   S.vers = A.vers;
@@ -297,6 +323,8 @@ Sched schedule(const Analysis& A, const Block& B, int la) {
     if (L.needed)
       for (const SRead& r : L.reads)
         if (crosses(B, r, A.dim)) shared[static_cast<size_t>(r.v)] = 1;
+  for (size_t vi = 0; vi < S.vers.size(); ++vi) S.vers[vi].xs = shared[vi] != 0;
+  const int imode = input_mode(A.dim);
   S.lag.assign(A.loops.size(), 0);
   for (size_t li = 0; li < A.loops.size(); ++li) {
     const SLoop& L = A.loops[li];
@@ -316,8 +344,9 @@ Sched schedule(const Analysis& A, const Block& B, int la) {
   for (size_t vi = 0; vi < S.vers.size(); ++vi) {
     SVer& v = S.vers[vi];
     if (v.prod >= 0 || !v.needed) continue;
-    v.tma = !v.pass_only && env_int("TCG_STREAM_TMA", 0) != 0;
-    const int lead = v.tma ? la : env_int("TCG_STREAM_REG_LEAD", A.dim == 2 ? 2 : 1);
+    v.tma = !v.pass_only && imode == 1;
+    v.cpa = !v.pass_only && imode == 2;
+    const int lead = v.async_in() ? la : env_int("TCG_STREAM_REG_LEAD", A.dim == 2 ? 2 : 1);
     v.lead = lead;
     int64_t lag = int64_t{1} << 40;
     for (size_t li = 0; li < A.loops.size(); ++li) {
@@ -340,10 +369,56 @@ Sched schedule(const Analysis& A, const Block& B, int la) {
     if (A.loops[li].needed) S.lmax = std::max(S.lmax, S.lag[li]);
   for (const SVer& v : S.vers)
     if (v.needed) S.lmax = std::max(S.lmax, v.lag);
+  // Own-point reads of versions staged in shared memory: from the shared ring
+  // (own_smem: no register ring, one LDS per read) or from a register ring.
+  // Shared-memory bandwidth is what bounds the generated kernels (profiles/r5:
+  // 62% of the crossbar on c2), so a register budget (doubles per point,
+  // TCG_STREAM_OWN_BUDGET) moves the versions with the most own-point reads
+  // per ring register back into registers.
+  for (SVer& v : S.vers) v.own_sm = B.own_smem;
+  if (B.own_smem) {
+    // Measured on c2 (profiles/r5/sweeps.md): 0.569 ms/step at 0, 0.552 at 16, 0.518 at 20-24 (164
+    // registers, still 3 CTAs/SM), 0.638 with every ring in registers (2 CTAs/SM).
+    int budget = env_int("TCG_STREAM_OWN_BUDGET", 20);
+    struct Cand {
+      size_t v;
+      int saved, cost;
+    };
+    std::vector<Cand> cands;
+    for (size_t vi = 0; vi < S.vers.size(); ++vi) {
+      const SVer& v = S.vers[vi];
+      if (!v.needed || !v.xs) continue;
+      int saved = 0;
+      int64_t amax = 0;
+      for (size_t li = 0; li < A.loops.size(); ++li) {
+        if (!A.loops[li].needed) continue;
+        for (const SRead& r : A.loops[li].reads) {
+          if (r.v != static_cast<int>(vi) || !in_block(B, r, A.dim, 0, 0)) continue;
+          const int64_t age = S.lag[li] - r.off[s] - v.lag;
+          if (v.async_in() || age >= 1) {
+            ++saved;
+            amax = std::max(amax, age);
+          }
+        }
+      }
+      const int cost = v.async_in() ? static_cast<int>(amax - v.lead + 1) : static_cast<int>(amax);
+      if (v.async_in()) --saved;  // the ring is filled by one shared-memory read per step
+      if (saved > 0 && cost > 0) cands.push_back(Cand{vi, saved, cost});
+    }
+    std::sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+      return a.saved * b.cost != b.saved * a.cost ? a.saved * b.cost > b.saved * a.cost : a.v < b.v;
+    });
+    for (const Cand& c : cands)
+      if (c.cost <= budget) {
+        S.vers[c.v].own_sm = false;
+        budget -= c.cost;
+      }
+  }
   // Ring depths per read source.
   for (SVer& v : S.vers) {
-    v.dr = 1;
+    v.dr = v.async_in() ? 0 : 1;
     v.ds = 0;
+    v.fill = false;
   }
   for (size_t li = 0; li < A.loops.size(); ++li) {
     const SLoop& L = A.loops[li];
@@ -355,7 +430,7 @@ Sched schedule(const Analysis& A, const Block& B, int la) {
       for (int jy = 0; jy < B.by; ++jy)
         for (int jx = 0; jx < B.bx; ++jx) {
           const bool blk = in_block(B, r, A.dim, jx, jy);
-          const bool sm = v.tma || !blk || (shared[static_cast<size_t>(r.v)] && B.own_smem && age >= 1);
+          const bool sm = read_via_smem(v, blk, age);
           if (sm) {
             if (age < 1) throw PlanError("stream executor: internal age error");
             v.ds = std::max<int>(v.ds, static_cast<int>(age) + 1);
@@ -363,6 +438,11 @@ Sched schedule(const Analysis& A, const Block& B, int la) {
               S.rx = std::max(S.rx, std::abs(static_cast<int>(r.off[0])));
               if (A.dim == 3) S.ry = std::max(S.ry, std::abs(static_cast<int>(r.off[1])));
             }
+          } else if (v.async_in()) {
+            // register ring over ages lead .. age, filled from shared memory
+            if (age < v.lead) throw PlanError("stream executor: internal lead error");
+            v.fill = true;
+            v.dr = std::max<int>(v.dr, static_cast<int>(age) - v.lead + 1);
           } else {
             v.dr = std::max<int>(v.dr, static_cast<int>(age) + 1);
           }
@@ -374,15 +454,14 @@ Sched schedule(const Analysis& A, const Block& B, int la) {
   // multiple when it is small, else depths padded to powers of two.
   S.la = la;
   S.ntma = 0;
+  S.ncpa = 0;
   for (SVer& v : S.vers) {
     if (!v.needed) continue;
     // A register-loaded shared input is staged into its ring at age lead-1.
-    if (v.prod < 0 && !v.tma && v.ds > 0) v.dr = std::max(v.dr, v.lead);
-    if (v.tma) {
-      v.dr = 0;
-      v.ds = std::max(v.ds, la + 1);
-      ++S.ntma;
-    }
+    if (v.prod < 0 && !v.async_in() && v.ds > 0) v.dr = std::max(v.dr, v.lead);
+    if (v.async_in()) v.ds = std::max(v.ds, la + 1);
+    if (v.tma) ++S.ntma;
+    if (v.cpa) ++S.ncpa;
   }
   S.nbar = S.ntma ? la + 1 : 0;
   auto lcm = [](int64_t a, int64_t b) {
@@ -466,7 +545,8 @@ Shape size_kernel(const Analysis& A, const LoopChain& ch, const StreamDevice& de
   int nloops = 0;
   for (const SLoop& L : A.loops) nloops += L.needed ? 1 : 0;
   const double lat_k = env_dbl("TCG_STREAM_LAT", 6.0);
-  const int la = env_int("TCG_STREAM_LOOKAHEAD", 2);
+  // cp.async lookahead: 2 rows in 2D (c2 0.518 -> 0.513 ms/step against 3: a smaller shared ring), 3 planes in 3D.
+  const int la = std::max(1, env_int("TCG_STREAM_LOOKAHEAD", input_mode(A.dim) == 2 && A.dim == 3 ? 3 : 2));
   Shape best;
   Sched best_sc;
   best.cost = 1e300;
@@ -477,8 +557,11 @@ Shape size_kernel(const Analysis& A, const LoopChain& ch, const StreamDevice& de
       Block B;
       B.bx = bx;
       B.by = by;
-      B.own_smem = A.dim == 2;
-      B.strided = A.dim == 2;
+      // 2D: one column per thread, strided by the CTA width when a thread has
+      // several; with TCG_STREAM_CONTIG2 (default on) bx > 1 means bx adjacent
+      // columns (16-byte shared-memory accesses, in-register x neighbours).
+      B.strided = A.dim == 2 && !(bx > 1 && bx % 2 == 0 && env_int("TCG_STREAM_CONTIG2", 1) != 0);
+      B.own_smem = A.dim == 2 && env_int("TCG_STREAM_OWN_SMEM", 1) != 0;
       auto it = scache.find({bx, by});
       if (it == scache.end()) it = scache.emplace(std::make_pair(bx, by), schedule(A, B, la)).first;
       const Sched& S0 = it->second;
@@ -493,7 +576,7 @@ Shape size_kernel(const Analysis& A, const LoopChain& ch, const StreamDevice& de
           if (P > 16) continue;
           S.tx = S.ntx * bx;
           S.ty = A.dim == 2 ? 1 : (nt / S.ntx) * by;
-          const int align = ((A.dim == 3 && bx > 1) || S0.ntma) ? 1 : 0;
+          const int align = ((!B.strided && bx > 1) || S0.ntma) ? 1 : 0;
           S.exl = A.E[0][0] + align;
           S.wox = S.tx - A.E[0][0] - A.E[0][1] - align;
           if (align) S.wox &= ~int64_t{1};
@@ -502,7 +585,7 @@ Shape size_kernel(const Analysis& A, const LoopChain& ch, const StreamDevice& de
           if (S.wox <= 0 || S.woy <= 0) continue;
           S.regs = est_regs(S0, P, nloops);
           if (S.regs > 255) continue;
-          S.rx = (A.dim == 2 && !S0.ntma) ? S0.rx : (S0.rx + 1) & ~1;
+          S.rx = (B.strided && !S0.ntma) ? S0.rx : (S0.rx + 1) & ~1;
           S.ry = S0.ry;
           S.spx = S.tx + 2 * S.rx;
           S.sp = static_cast<int64_t>(S.spx) * (S.ty + 2 * S.ry);
@@ -622,7 +705,7 @@ struct Gen {
     const int ox = r.pass ? 0 : static_cast<int>(r.off[0]);
     const int oy = r.pass ? 0 : (A.dim == 3 ? static_cast<int>(r.off[1]) : 0);
     const bool blk = in_block(S.blk, r, A.dim, jx(j), jy(j));
-    const bool sm = v.tma || !blk || (is_shared(r.v) && S.blk.own_smem && age >= 1);
+    const bool sm = read_via_smem(v, blk, age);
     if (!sm) {
       const int tj = (jy(j) + oy) * S.blk.bx + (jx(j) + ox);
       return "V" + std::to_string(r.v) + "[" + std::to_string(reg_slot(r.v, u, age)) + "][" + std::to_string(tj) + "]";
@@ -685,6 +768,18 @@ __device__ __forceinline__ void pf_l2(const double* p, long long n) {
   const unsigned long long a1 = (reinterpret_cast<unsigned long long>(p + n) + 15ULL) & ~15ULL;
   if (a1 > a0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
 }
+__device__ __forceinline__ unsigned su32(const void* p);
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ double nanv() { return __longlong_as_double(0x7ff8dead00000000LL); }
 __device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
@@ -719,7 +814,8 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
   const int U = Sc.unroll;
   const int nd = static_cast<int>(A.dats.size());
   const int BX = S.blk.bx;
-  const bool vec = A.dim == 3 && BX % 2 == 0;  // contiguous x pairs: 16-byte accesses
+  const bool contig = !S.blk.strided;
+  const bool vec = contig && BX % 2 == 0;  // contiguous x pairs: 16-byte accesses
   for (int k = 0; k < nd; ++k) {
     const StreamGeom& G = geoms.at(static_cast<size_t>(A.dats[static_cast<size_t>(k)]));
     int found = -1;
@@ -782,13 +878,13 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
     << " / A.ns), s1 = " << hs0 << " + static_cast<int>(static_cast<long long>(iseg + 1) * " << (hs1 - hs0)
     << " / A.ns);\n";
   // Tile origin X0 (even when rows are bulk-copied or paired: 16-byte alignment).
-  if ((A.dim == 3 && BX > 1) || Sc.ntma)
+  if ((contig && BX > 1) || Sc.ntma)
     o << "  const int X0 = (ox0 - " << (S.exl - 1) << ") & ~1;\n";
   else
     o << "  const int X0 = ox0 - " << S.exl << ";\n";
-  o << "  const int cx0 = X0 + " << (A.dim == 3 ? "tx * BX" : "tid") << ";\n";
+  o << "  const int cx0 = X0 + " << (contig ? "tx * BX" : "tid") << ";\n";
   o << "  const int cy0 = " << (A.dim == 3 ? "oy0 - " + std::to_string(S.eyl) + " + ty * BY" : std::string("0")) << ";\n";
-  if (A.dim == 3)
+  if (contig)
     o << "  double* const smp = sm + (ty * BY + " << S.ry << ") * SPX + tx * BX + " << S.rx << ";\n";
   else
     o << "  double* const smp = sm + tid + " << S.rx << ";\n";
@@ -800,9 +896,10 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
     if (A.dim == 3) o << " + static_cast<long long>(cy0 - " << q.y0 << ") * " << fmt_L(q.py);
     o << ";\n";
   }
-  std::vector<int> loaded, tma;
+  std::vector<int> loaded, tma, cpa;
   for (size_t v = 0; v < Sc.vers.size(); ++v)
-    if (Sc.vers[v].needed && Sc.vers[v].prod < 0) (Sc.vers[v].tma ? tma : loaded).push_back(static_cast<int>(v));
+    if (Sc.vers[v].needed && Sc.vers[v].prod < 0)
+      (Sc.vers[v].tma ? tma : (Sc.vers[v].cpa ? cpa : loaded)).push_back(static_cast<int>(v));
   const int rows_per = A.dim == 3 ? S.ty : 1;
   const int nrows = static_cast<int>(tma.size()) * rows_per;  // bulk copies per step
   const int nissue = std::min(nrows, S.nt);                     // threads issuing them
@@ -904,6 +1001,37 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
         ++idx;
       }
     }
+    // cp.async: every thread copies its points of the input row t - lag into
+    // the shared ring (read from `la` steps on); one group per step.
+    for (int v : cpa) {
+      const SVer& sv = Sc.vers[static_cast<size_t>(v)];
+      const int c = g.slot_gc[static_cast<size_t>(sv.slot)];
+      const Gen::GC& q = g.gcs[static_cast<size_t>(c)];
+      const int am = g.box_id(q.alloc);
+      const int64_t so = g.sm_slot_off(v, u, 0);
+      const int64_t ro = spitch(q) * u;
+      body << "    { // cp.async version " << v << " (slot " << sv.slot << ")\n";
+      body << "      const int r = t - " << sv.lag << ";\n";
+      body << "      const double* __restrict__ lp" << v << " = A.src[" << sv.slot << "] + (rb" << c << " - "
+           << fmt_L(spitch(q) * sv.lag) << ");\n";
+      body << "      if (t + " << Sc.la << " < tend && r >= " << q.alloc.start(s) << " && r < " << q.alloc.end(s) << ") {\n";
+      for (int j = 0; j < P; ++j) {
+        const int64_t off = ro + g.g_off(q, j);
+        if (vec && g.jx(j) % 2 == 0) {
+          body << "        if (((m" << am << " >> " << j << ") & 3u) == 3u) tcgj::cp_async16(&smp[" << (so + g.sm_off(j)) << "], lp"
+               << v << " + " << off << ");\n";
+          body << "        else { if ((m" << am << " >> " << j << ") & 1u) tcgj::cp_async8(&smp[" << (so + g.sm_off(j)) << "], lp" << v
+               << " + " << off << "); if ((m" << am << " >> " << (j + 1) << ") & 1u) tcgj::cp_async8(&smp["
+               << (so + g.sm_off(j + 1)) << "], lp" << v << " + " << (off + 1) << "); }\n";
+          ++j;
+        } else {
+          body << "        if ((m" << am << " >> " << j << ") & 1u) tcgj::cp_async8(&smp[" << (so + g.sm_off(j)) << "], lp" << v
+               << " + " << off << ");\n";
+        }
+      }
+      body << "      }\n    }\n";
+    }
+    if (!cpa.empty()) body << "    tcgj::cp_async_commit();\n";
     // loads: the input row t - lag lands in register age 0
     for (int v : loaded) {
       const SVer& sv = Sc.vers[static_cast<size_t>(v)];
@@ -946,6 +1074,15 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
       }
       body << "      }\n    }\n";
     }
+    // Whole-step interior path (TCG_STREAM_FAST): when every loop's row is in
+    // range and every point of the thread is inside every loop's range, the
+    // step is one straight-line block -- no per-loop range branches or
+    // pass-through selects -- so the compiler overlaps the shared-memory
+    // reads and the fp64 chains of all loops.
+    // Measured on B200 (profiles/r5): slower in 2D (c2 0.56 -> 0.70 ms/step: the long step body doubles),
+    // neutral in 3D; off by default.
+    const bool step_fast = env_int(A.dim == 2 ? "TCG_STREAM_FAST2" : "TCG_STREAM_FAST3", env_int("TCG_STREAM_FAST", 0)) != 0;
+    auto emit_loops = [&](bool all_fast) {
     size_t racc = 0;
     for (size_t li = 0; li < ch.loops.size(); ++li) {
       const SLoop& Lp = A.loops[li];
@@ -1059,7 +1196,9 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
         body << "      }\n";
       }
       };
-      if (has_pass && A.dim == 3) {
+      if (all_fast) {
+        emit_points(true);
+      } else if (has_pass && A.dim == 3) {
         // Interior fast path (3D; measured slower in 2D): every point of the thread inside the loop's
         // range this row -- no pass-through selects.
         body << "      if (rin && m" << rb << " == " << ((1u << P) - 1u) << "u) {\n";
@@ -1105,6 +1244,28 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
       }
       body << "    }\n";
     }
+    };
+    if (step_fast) {
+      std::set<int> rbs;
+      body << "    if (";
+      bool first = true;
+      for (size_t li = 0; li < ch.loops.size(); ++li) {
+        if (!A.loops[li].needed) continue;
+        const LoopRecord& lp = ch.loops[li];
+        rbs.insert(g.box_id(lp.range));
+        body << (first ? "" : " && ") << "(t - " << Sc.lag[li] << ") >= " << g.s_lo(lp.range) << " && (t - " << Sc.lag[li]
+             << ") < " << g.s_hi(lp.range);
+        first = false;
+      }
+      for (int rb : rbs) body << " && m" << rb << " == " << ((1u << P) - 1u) << "u";
+      body << ") {\n";
+      emit_loops(true);
+      body << "    } else {\n";
+      emit_loops(false);
+      body << "    }\n";
+    } else {
+      emit_loops(false);
+    }
     // inputs enter their shared ring at age la-1 (read from age la on)
     for (int v : loaded)
       if (g.is_shared(v)) stage_store(body, v, u, Sc.vers[static_cast<size_t>(v)].lead - 1, "    ");
@@ -1117,7 +1278,24 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
       steps << "    if (t - " << Sc.la << " >= tstart) tcgj::mbar_wait(&bar[" << (((u - Sc.la) % Sc.nbar + Sc.nbar) % Sc.nbar)
             << "], static_cast<unsigned>(((t - " << Sc.la << " - tstart) / " << Sc.nbar << ") & 1));\n";
     }
+    if (!cpa.empty()) steps << "    tcgj::cp_async_wait<" << (Sc.la - 1) << ">();\n";
     steps << "    __syncthreads();\n";
+    // asynchronous inputs: the row that becomes readable this step enters the register ring
+    for (size_t v = 0; v < Sc.vers.size(); ++v) {
+      const SVer& sv = Sc.vers[v];
+      if (!sv.needed || sv.prod >= 0 || !sv.async_in() || !sv.fill || sv.dr == 0) continue;
+      const int rs = g.reg_slot(static_cast<int>(v), u, sv.lead);
+      const int64_t so = g.sm_slot_off(static_cast<int>(v), u, sv.lead);
+      for (int j = 0; j < P; ++j) {
+        if (vec && g.jx(j) % 2 == 0) {
+          steps << "    { const double2 q = *reinterpret_cast<const double2*>(&smp[" << (so + g.sm_off(j)) << "]); V" << v << "["
+                << rs << "][" << j << "] = q.x; V" << v << "[" << rs << "][" << (j + 1) << "] = q.y; }\n";
+          ++j;
+        } else {
+          steps << "    V" << v << "[" << rs << "][" << j << "] = smp[" << (so + g.sm_off(j)) << "];\n";
+        }
+      }
+    }
     emit_step(steps, u);
     steps << "    }\n    }\n";
   }
@@ -1146,6 +1324,7 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
   o << steps.str();
   o << adv.str();
   o << "  }\n";
+  if (Sc.ncpa) o << "  tcgj::cp_async_wait<0>();\n";  // nothing may land in the reduction scratch
   if (!accs.empty()) {
     const int nw = S.nt / 32;
     o << "  __syncthreads();\n";
@@ -1223,7 +1402,10 @@ int64_t StreamKernel::segments_for(int64_t slots) const {
   if (forced_segments > 0) return std::min<int64_t>(forced_segments, stream_extent);
   // One wave when the tiles leave room (floor: never one CTA past a wave),
   // segments long against the pipeline warm-up.
-  int64_t ns = tiles >= slots ? 1 : slots / tiles;
+  // More tiles than resident slots: several waves. A few segments per tile
+  // even out the last wave (c3, 400 tiles on 148 SMs: 7.60 ms/chain with 1
+  // segment, 6.95 with 3, 6.83 with 4; profiles/r5/sweeps.md).
+  int64_t ns = tiles >= slots ? (dim == 3 ? 4 : 1) : slots / tiles;
   ns = std::min<int64_t>(ns, std::max<int64_t>(1, stream_extent / min_seg));
   return std::max<int64_t>(1, ns);
 }

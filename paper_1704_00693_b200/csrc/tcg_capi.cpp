@@ -249,6 +249,22 @@ int tcg_stream_plan_pending(tcg_runtime* rt, int what, char* buf, int64_t n, int
   });
 }
 
+int tcg_periodic_plan_pending(tcg_runtime* rt, char* buf, int64_t n, int64_t* needed) {
+  return guard([&] {
+    tcg::LoopChain c = rt->rt->take_pending();
+    std::vector<tcg::Range> logical;
+    for (size_t i = 0; i < rt->rt->num_fields(); ++i) logical.push_back(rt->rt->logical_range(static_cast<tcg::DatasetId>(i)));
+    const tcg::PeriodicPlan p = tcg::apply_periodic(c, logical);
+    std::ostringstream os;
+    os << "loops=" << p.chain.size() << " marks=" << c.fills.size() << " max_extension=" << p.max_extension
+       << " extended_points=" << p.extended_points << "\n";
+    for (size_t l = 0; l < p.chain.size(); ++l)
+      os << "loop=" << l << " " << c.loops[l].kernel.name << " range=" << p.chain.loops[l].range.to_string() << "\n";
+    for (const auto& [ds, depth] : p.pre_fills) os << "wrap ds=" << ds << " depth=" << depth << "\n";
+    put_text(os.str(), buf, n, needed);
+  });
+}
+
 int tcg_plan_pending(tcg_runtime* rt, const int64_t ts[3], char* buf, int64_t n, int64_t* needed) {
   return guard([&] {
     tcg::LoopChain c = rt->rt->take_pending();
@@ -355,6 +371,25 @@ int tcg_local_box(tcg_runtime* rt, int32_t ds, int64_t out[6]) {
       out[2 * d + 1] = d < b.dim() ? b.end(d) : 1;
     }
   });
+}
+
+int tcg_record_begin(tcg_runtime* rt) {
+  return guard([&] { rt->rt->record_begin(); });
+}
+int tcg_record_end(tcg_runtime* rt, int32_t* id) {
+  return guard([&] { *id = rt->rt->record_end(); });
+}
+int tcg_replay(tcg_runtime* rt, int32_t id, const double* params, int64_t nparams, int32_t* handles, int64_t max_handles,
+               int64_t* nhandles) {
+  return guard([&] {
+    const std::vector<tcg::ReductionHandle> hs = rt->rt->replay(id, params, params ? static_cast<size_t>(nparams) : 0);
+    if (nhandles) *nhandles = static_cast<int64_t>(hs.size());
+    for (size_t i = 0; i < hs.size() && static_cast<int64_t>(i) < max_handles; ++i) handles[i] = hs[i].id;
+  });
+}
+
+int tcg_set_periodic_flush(tcg_runtime* rt, int flush_each) {
+  return guard([&] { rt->rt->set_periodic_flush(flush_each != 0); });
 }
 
 int tcg_periodic_fill(tcg_runtime* rt, int n, const int32_t* ds, int64_t depth) {

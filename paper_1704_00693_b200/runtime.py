@@ -107,6 +107,12 @@ def load_library() -> ctypes.CDLL:
         "tcg_stream_plan_pending": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_char_p, _I64, ctypes.POINTER(_I64)]),
         "tcg_set_rank_grid": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
         "tcg_periodic_fill": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I32), _I64]),
+        "tcg_set_periodic_flush": (ctypes.c_int, [_P, ctypes.c_int]),
+        "tcg_record_begin": (ctypes.c_int, [_P]),
+        "tcg_record_end": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
+        "tcg_replay": (ctypes.c_int, [_P, _I32, ctypes.POINTER(ctypes.c_double), _I64, ctypes.POINTER(_I32), _I64,
+                                      ctypes.POINTER(_I64)]),
+        "tcg_periodic_plan_pending": (ctypes.c_int, [_P, ctypes.c_char_p, _I64, ctypes.POINTER(_I64)]),
         "tcg_upload_box": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_I64)]),
         "tcg_download_box": (ctypes.c_int, [_P, _I32, _P, ctypes.POINTER(_I64)]),
         "tcg_local_box": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_I64)]),
@@ -510,13 +516,47 @@ class Runtime:
 
     def periodic_fill(self, datasets, depth: int, logical=None) -> None:
         """Periodic ghost layers (depth <= pad) for every listed field, over
-        each field's logical box (`logical`, if given, must equal it); flushes."""
+        each field's logical box (`logical`, if given, must equal it).
+        Recorded in the queue (the chain is rewritten at flush: one wrap per
+        chain, loops extended into the ghost layers); set_periodic_flush(True)
+        makes it flush and copy at once."""
         ds = list(datasets)
         if logical is not None:
             for d in ds:
                 if list(self._logicals[d].lohi[: 2 * self.dim]) != list(logical)[: 2 * self.dim]:
                     raise InvalidArgument("periodic_fill: box differs from the field's logical range")
         _check(self._lib.tcg_periodic_fill(self._h, len(ds), _arr(_I32, ds), depth))
+
+    def periodic_plan_pending(self) -> str:
+        """Host-only: the pending chain rewritten around its periodic marks."""
+        return _text(self._lib.tcg_periodic_plan_pending, self._h)
+
+    # ---- step templates ------------------------------------------------------
+    def record_begin(self) -> None:
+        """Keep the par_loop / periodic_fill calls made until record_end as a
+        template (they are enqueued normally too)."""
+        _check(self._lib.tcg_record_begin(self._h))
+
+    def record_end(self) -> int:
+        out = _I32(0)
+        _check(self._lib.tcg_record_end(self._h, ctypes.byref(out)))
+        return out.value
+
+    def replay(self, template: int, params=None):
+        """Issue the recorded calls again (C++ host path, one binding crossing);
+        `params` replaces the kernels' scalars in call order. Returns the new
+        reduction handles."""
+        hs = (_I32 * 16)()
+        n = _I64(0)
+        if params is None:
+            _check(self._lib.tcg_replay(self._h, template, None, 0, hs, 16, ctypes.byref(n)))
+        else:
+            arr = (ctypes.c_double * len(params))(*params)
+            _check(self._lib.tcg_replay(self._h, template, arr, len(params), hs, 16, ctypes.byref(n)))
+        return [hs[i] for i in range(min(n.value, 16))]
+
+    def set_periodic_flush(self, flush_each: bool) -> None:
+        _check(self._lib.tcg_set_periodic_flush(self._h, 1 if flush_each else 0))
 
     def upload_box(self, ds: int, data: np.ndarray, box: Range) -> None:
         arr = np.ascontiguousarray(data, dtype=np.float64)

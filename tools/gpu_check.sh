@@ -9,7 +9,7 @@ for c in ${CONFIGS:-c2 c3 c1}; do
     python - $OUT/bench_${c}_$m.json <<'PY'
 import json,sys
 try:
-    d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); p=d['config']['plan']
+    d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); p=d['detail']['plan']
     print(f"{sys.argv[1].split('/')[-1]:28s} ms/step={d['ms_per_step']:.4f} exec={p['executor']} ctas={p['ctas']} sub={p['subchains']} frac={d['roofline'].get('frac')}")
 except Exception as e: print(sys.argv[1], 'ERR', e)
 PY

@@ -11,7 +11,7 @@ run() { # config tag cfg [env...]
   python - $OUT/${c}_$tag.json "$cfg" <<'PY'
 import json,sys
 try:
-    d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); p=d['config']['plan']
+    d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); p=d['detail']['plan']
     print(f"{sys.argv[1].split('/')[-1]:28s} cfg={sys.argv[2]:24s} ms/step={d['ms_per_step']:.4f} ctas={p['ctas']} sub={p['subchains']} tile={p['tile_sizes']} frac={d['roofline'].get('frac')}")
 except Exception as e: print(sys.argv[1], 'ERR', e)
 PY
