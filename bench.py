@@ -231,11 +231,11 @@ WORKLOAD_TEXT = {
 }
 
 
+SHARDED = {"c2": 1, "c3": 2}  # config -> dimension its domain is split along at N > 1
+
+
 def workload_text(name, world):
-    t = WORKLOAD_TEXT[name]
-    if name == "c2" and world > 1:
-        t = t.replace("fp64 4096^2", f"fp64 4096 x {4096 * world} (one 4096^2 slab per GPU, weak scaling)")
-    return t
+    return WORKLOAD_TEXT[name]
 
 
 def parse_mode(s):
@@ -280,10 +280,12 @@ def max_over_ranks(v, dist):
 
 def config_dict(name, world):
     """The workload description both arms print (identical by construction)."""
-    sharded = world > 1 and name == "c2"
+    sharded = world > 1 and name in SHARDED
     return {"workload": workload_text(name, world),
-            "parallelism": (f"{world} y-slabs of 4096^2 (domain 4096x{4096 * world}), one deep-halo exchange per "
-                            "chain" if sharded else ("replicas" if world > 1 else "single GPU")),
+            "parallelism": (f"the BASELINE domain split into {world} slabs along {'xyz'[SHARDED[name]]} (strong "
+                            "scaling), one rank per GPU, one deep-halo exchange per chain (NCCL send/recv of whole "
+                            "rows / planes straight from the fields)" if sharded else
+                            ("independent replicas" if world > 1 else "single GPU")),
             "l2": "inputs exceed the 126 MB L2; no flush needed"}
 
 
@@ -350,14 +352,14 @@ def cpu_reference(cfg_name, k, warmup, budget_s=120.0, mode_pick=None, ny=None):
 def run_reference_arm(args, world, rank, dist):
     if rank != 0:
         return 0
-    # Same workload as the B200 arm: at N > 1 c2 is the 4096 x 4096N domain.
-    ny = 4096 * world if (world > 1 and args.config == "c2") else None
-    res, err = cpu_reference(args.config, args.steps + args.warmup, args.warmup, budget_s=args.ref_budget, ny=ny)
+    # Same workload as the B200 arm: the BASELINE domain (split across the GPUs there).
+    res, err = cpu_reference(args.config, args.steps + args.warmup, args.warmup, budget_s=args.ref_budget)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": err}))
         return 0
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong" if (world > 1 and args.config in SHARDED) else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE shapes)",
             "config": config_dict(args.config, world), "impl": "reference", "cpu_baseline": res,
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -404,10 +406,11 @@ def main():
     torch.cuda.set_device(local)
     mode = parse_mode(args.mode)
 
-    # N > 1: c2 is decomposed into one 4096^2 slab per GPU along y (weak
-    # scaling, domain 4096 x 4096N) with one deep-halo exchange per chain over
-    # NCCL; the other configs run as independent replicas.
-    sharded = (world > 1 or args.shard) and args.config == "c2"
+    # N > 1: c2 (along y) and c3 (along z) split the BASELINE domain across the
+    # GPUs -- strong scaling, one rank per process, one deep-halo exchange per
+    # chain over NCCL; c1 / c4 / c5 run as independent replicas (c5's periodic
+    # wrap is not available on a rank grid yet).
+    sharded = (world > 1 or args.shard) and args.config in SHARDED
 
     def new_comm_id():
         # One NCCL unique id per communicator (every runtime gets its own).
@@ -419,9 +422,11 @@ def main():
     def build(m):
         rt = Runtime(3 if args.config in ("c3", "c5") else 2)
         if sharded:
-            rt.set_process_rank((1, world, 1), rank, new_comm_id())
+            grid = [1, 1, 1]
+            grid[SHARDED[args.config]] = world
+            rt.set_process_rank(tuple(grid), rank, new_comm_id())
         rt.set_default_mode(m)
-        cfg = make_config(args.config, rt, ny=4096 * world if sharded else None)
+        cfg = make_config(args.config, rt)
         return rt, cfg, Step(args.config, cfg, rt, host=args.host)
 
     # ---- device-resident throughput (value) ----------------------------------
@@ -557,7 +562,8 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong" if (sharded and world > 1) else "weak",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic: seeded PCG64 fields with the BASELINE config shapes and value ranges",
                 "config": config_dict(args.config, world),

@@ -110,6 +110,11 @@ int tcg_pending_loops(tcg_runtime* rt, int64_t* out);
  * reference's C++ apps do every step (apps.cpp:59-130, :163-254), in one
  * crossing of the binding. params (may be NULL) replaces the kernels' scalar
  * parameters in call order. Returns the new reduction handles in call order. */
+/* Sum reductions folded in the reference's order for RuntimeConfig::threads =
+ * workers (executor.cpp:55-61, :141-144, :175-176): such chains run untiled,
+ * every point's contribution is captured and summed sequentially over the
+ * reference's static spans, partials folded in worker order. 0 = fast fold. */
+int tcg_set_reduction_order(tcg_runtime* rt, int workers);
 int tcg_record_begin(tcg_runtime* rt);
 int tcg_record_end(tcg_runtime* rt, int32_t* id);
 int tcg_replay(tcg_runtime* rt, int32_t id, const double* params, int64_t nparams, int32_t* handles,

@@ -40,13 +40,18 @@ struct ULaunch {
   double prm[kMaxParams];
   DevStencils st;
   double* partials;
+  // Order-matched Sum (DeviceExec::set_reduction_workers): every point's
+  // contribution is stored here at its memory-order index within the loop
+  // range instead of being folded by the thread.
+  double* capture;
   // L2 prefetch of the block's read footprint (0 = off): union of the read
   // stencils' offsets per dimension, and the mask of arguments that read.
   int32_t pf, rmask;
   int32_t rlo[3], rhi[3];
   // Staged 3D walk (k_untiled3s): tile rows (TY) and planes per block (ZR),
   // shared-memory ring base (doubles) of each reading argument.
-  int32_t sty, szr, sslots, pad3_;
+  int32_t sty, szr, sslots;
+  int32_t band;  // 3D: y-blocks per rasterisation band (block_yz), 0 = hardware order
   int32_t sring[kMaxArgs];
 #ifdef TCG_CHECKED
   int64_t alo[kMaxArgs][3], ahi[kMaxArgs][3];  // allocation of each argument
@@ -91,6 +96,33 @@ __device__ __noinline__ void checked_access(const ULaunch& L, int a, int dx, int
 // is computed: the block's DRAM misses are then all in flight at once
 // instead of one plane / row at a time behind the dependent loads (the 3D
 // walk was measured long-scoreboard bound at 46% occupancy).
+// 3D block order. The hardware walks blockIdx x-fastest, then y, then z: two
+// z-chunks of the same column run a whole plane-chunk apart (c5: 6 fields x
+// 4 planes x 4.7 MB = 113 MB, the size of L2), so the z-halo planes of the
+// radius-2 stars were re-read from HBM (2.09x read amplification on the
+// energy RHS, profiles/r3/c5_untiled.md). With a band of L.band y-blocks the
+// linear (y, z) index is re-read as (y inside the band, z-chunk, band): a
+// column's z-chunks follow each other within one band, and only the band's
+// edge rows are fetched twice.
+__device__ __forceinline__ void block_yz(const ULaunch& L, unsigned& by, unsigned& bz) {
+  by = blockIdx.y;
+  bz = blockIdx.z;
+  const unsigned band = static_cast<unsigned>(L.band);
+  if (band == 0 || band >= gridDim.y) return;
+  const unsigned ny = gridDim.y, nz = gridDim.z;
+  const unsigned lin = blockIdx.y + ny * blockIdx.z;
+  const unsigned full = (ny / band) * band * nz;  // blocks in whole bands
+  if (lin < full) {
+    const unsigned b = lin / (band * nz), r = lin - b * band * nz;
+    bz = r / band;
+    by = b * band + (r - bz * band);
+  } else {
+    const unsigned w = ny % band, r = lin - full;
+    bz = r / w;
+    by = (ny / band) * band + (r - bz * w);
+  }
+}
+
 template <int DIM, int RUN>
 __device__ __forceinline__ void prefetch_footprint(const ULaunch& L) {
   const int64_t xe = L.lo[0] + L.n[0], ye = L.lo[1] + L.n[1], ze = L.lo[2] + L.n[2];
@@ -103,9 +135,11 @@ __device__ __forceinline__ void prefetch_footprint(const ULaunch& L) {
     z0 = 0;
     z1 = 1;
   } else {
-    y0 = L.lo[1] + static_cast<int64_t>(blockIdx.y) * blockDim.y;
+    unsigned by, bz;
+    block_yz(L, by, bz);
+    y0 = L.lo[1] + static_cast<int64_t>(by) * blockDim.y;
     y1 = min(y0 + static_cast<int64_t>(blockDim.y), ye);
-    z0 = L.lo[2] + static_cast<int64_t>(blockIdx.z) * RUN;
+    z0 = L.lo[2] + static_cast<int64_t>(bz) * RUN;
     z1 = min(z0 + static_cast<int64_t>(RUN), ze);
   }
   if (x0 >= x1 || y0 >= y1 || z0 >= z1) return;
@@ -175,6 +209,10 @@ struct GAcc {
     if (L.masked && (px < L.mlo[0] || px >= L.mhi[0] || py < L.mlo[1] || py >= L.mhi[1] || pz < L.mlo[2] ||
                      pz >= L.mhi[2]))
       return;
+    if (L.capture) {
+      L.capture[((pz - L.lo[2]) * L.n[1] + (py - L.lo[1])) * L.n[0] + (px - L.lo[0])] = v;
+      return;
+    }
     acc = red_combine(L.red_op, acc, v);
   }
   __device__ __forceinline__ int nargs() const { return L.nargs; }
@@ -185,6 +223,43 @@ struct GAcc {
   }
   __device__ __forceinline__ bool reduces() const { return L.has_red != 0; }
 };
+
+// Order-matched Sum, the reference's fold (executor.cpp:55-61 slice,
+// :141-144 per-worker partials from the identity, :175-176 worker-order
+// fold): block w sums span w of the captured contributions sequentially --
+// the block stages chunks through shared memory, thread 0 adds them in index
+// order -- and the last block to finish folds the T partials in worker order.
+__global__ void __launch_bounds__(256) k_ordered_sum(const double* __restrict__ vals, int64_t n, int workers, double* part,
+                                                     unsigned* ticket, double* out) {
+  constexpr int kChunk = 2048;
+  __shared__ double buf[kChunk];
+  const int64_t T = workers, w = blockIdx.x;
+  const int64_t base = n / T, rem = n % T;
+  const int64_t begin = w * base + (w < rem ? w : rem);
+  const int64_t end = begin + base + (w < rem ? 1 : 0);
+  double acc = 0.0;  // reduce_identity(Sum)
+  for (int64_t c = begin; c < end; c += kChunk) {
+    const int m = static_cast<int>(end - c < kChunk ? end - c : kChunk);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) buf[i] = __ldg(vals + c + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll 8
+      for (int i = 0; i < m; ++i) acc = acc + buf[i];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[w] = acc;
+    __threadfence();
+    if (atomicAdd(ticket, 1u) == static_cast<unsigned>(workers) - 1) {
+      __threadfence();
+      double r = 0.0;
+      for (int i = 0; i < workers; ++i) r = r + __ldcg(part + i);
+      *out = r;
+      *ticket = 0u;
+    }
+  }
+}
 
 // Two-pass run for bodies whose reads are few and in a data-independent order
 // but whose arithmetic holds a branchy IEEE division (c2's CFL min-reduction,
@@ -265,8 +340,10 @@ __device__ __forceinline__ void untiled_block(const ULaunch& L) {
       rend = L.lo[1] + L.n[1];
       acc.py = r0;
     } else {
-      acc.py = L.lo[1] + static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
-      r0 = L.lo[2] + static_cast<int64_t>(blockIdx.z) * kUntiledRun;
+      unsigned by, bz;
+      block_yz(L, by, bz);
+      acc.py = L.lo[1] + static_cast<int64_t>(by) * blockDim.y + threadIdx.y;
+      r0 = L.lo[2] + static_cast<int64_t>(bz) * kUntiledRun;
       rend = L.lo[2] + L.n[2];
       acc.pz = r0;
     }
@@ -590,6 +667,7 @@ DeviceExec::DeviceExec() {
   TCG_CK(cudaGetDeviceCount(&ndev));
   if (ndev <= 0) throw CudaError("no CUDA device visible: the B200 executor has no CPU fallback");
   TCG_CK(cudaGetDevice(&info_.device));
+  device_ = info_.device;
   cudaDeviceProp prop;
   TCG_CK(cudaGetDeviceProperties(&prop, info_.device));
   info_.num_sms = prop.multiProcessorCount;
@@ -628,6 +706,9 @@ DeviceExec::~DeviceExec() {
   if (st_part_) cudaFree(st_part_);
   if (st_out_) cudaFree(st_out_);
   if (st_ticket_) cudaFree(st_ticket_);
+  if (capture_) cudaFree(capture_);
+  if (ord_part_) cudaFree(ord_part_);
+  if (ord_ticket_) cudaFree(ord_ticket_);
   if (host_stage_) cudaFreeHost(host_stage_);
   drop_graphs();
   if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
@@ -1031,6 +1112,8 @@ struct ULaunchRec {
   unsigned smem;  // dynamic shared memory (staged 3D walk)
   int64_t nblocks;
   int red;  // >= 0: followed by k_fold into red_dev_[red]
+  bool ordered = false;  // Sum folded by k_ordered_sum over the captured contributions
+  int64_t volume = 0;
 };
 
 uint64_t launch_key(const std::vector<ULaunchRec>& recs, int dim) {
@@ -1161,6 +1244,7 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
     }
     L.st = cd.st;
     L.pf = prefetch ? 1 : 0;
+
     // Planes per thread in 3D: 8 for small stencils (c3's 7 points: the
     // z-neighbours of 8 planes stay in registers), 4 when the loop reads
     // more than 8 stencil points in total (c5's radius-2 RHS loops: 8 planes
@@ -1183,6 +1267,15 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
           L.rhi[d] = std::max(L.rhi[d], ch.st_pts[static_cast<size_t>(3 * (s0 + j) + d)]);
         }
     }
+    // Rasterisation band (block_yz): measured on B200 (profiles/r5/sweeps.md) -- c5's radius-2 loops
+    // 283.9 ms/step in hardware order, 275.1 with 64-block bands (-3%); c3's 7-point sweeps (8 planes
+    // per thread, reach 1) lose 11% with any band, so only loops reaching >= 2 planes are banded.
+    // TCG_UNTILED_BAND overrides (0 = hardware order everywhere).
+    static const int band_env = [] {
+      const char* e = std::getenv("TCG_UNTILED_BAND");
+      return e && *e ? std::atoi(e) : -1;
+    }();
+    L.band = ch.dim == 3 ? (band_env >= 0 ? band_env : (L.rhi[2] - L.rlo[2] >= 4 ? 64 : 0)) : 0;
     if (ch.dim == 1) {
       R.block = dim3(256, 1, 1);
       R.grid = dim3(static_cast<unsigned>(std::max<int64_t>(1, (n[0] + 255) / 256)), 1, 1);
@@ -1230,6 +1323,11 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
     }
     R.nblocks = static_cast<int64_t>(R.grid.x) * R.grid.y * R.grid.z;
     R.red = L.has_red ? lp.red : -1;
+    if (L.has_red && red_workers_ > 0 && L.red_op == tcb::kSum && !empty) {
+      if (L.masked) throw InvalidArgument("order-matched Sum: not available for rank-masked reductions");
+      R.ordered = true;
+      R.volume = n[0] * n[1] * n[2];
+    }
     if (empty) {
       if (L.has_red) {
         // Empty reducing loop: the result is the identity.
@@ -1280,7 +1378,34 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
       if (r.red >= 0) r.L.partials = part + (i++) * max_blocks;
   }
 
-  const bool graph_ok = use_graphs && !timing_ && !empty_red && !recs.empty();
+  // Order-matched Sums: one capture region per such loop, then the
+  // reference's span partition and worker-order fold (k_ordered_sum).
+  bool any_ordered = false;
+  {
+    size_t total = 0;
+    for (const ULaunchRec& r : recs) total += r.ordered ? static_cast<size_t>(r.volume) : 0;
+    if (total > 0) {
+      any_ordered = true;
+      if (total > capture_n_) {
+        TCG_CK(cudaStreamSynchronize(st));
+        if (capture_) TCG_CK(cudaFree(capture_));
+        capture_n_ = total;
+        TCG_CK(cudaMalloc(&capture_, capture_n_ * sizeof(double)));
+      }
+      if (!ord_part_) {
+        TCG_CK(cudaMalloc(&ord_part_, sizeof(double) * 1024));
+        TCG_CK(cudaMalloc(&ord_ticket_, sizeof(unsigned)));
+        TCG_CK(cudaMemsetAsync(ord_ticket_, 0, sizeof(unsigned), st));
+      }
+      size_t off = 0;
+      for (ULaunchRec& r : recs)
+        if (r.ordered) {
+          r.L.capture = capture_ + off;
+          off += static_cast<size_t>(r.volume);
+        }
+    }
+  }
+  const bool graph_ok = use_graphs && !timing_ && !empty_red && !recs.empty() && !any_ordered;
   if (graph_ok) {
     const uint64_t key = launch_key(recs, ch.dim);
     UGraph* g = nullptr;
@@ -1364,7 +1489,12 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
         ev_untiled_.emplace_back(e0, e1);
       }
       ++launches_;
-      if (r.red >= 0) {
+      if (r.ordered) {
+        k_ordered_sum<<<red_workers_, 256, 0, st>>>(r.L.capture, r.volume, red_workers_, ord_part_, ord_ticket_,
+                                                    red_dev_ + r.red);
+        TCG_CK(cudaGetLastError());
+        ++launches_;
+      } else if (r.red >= 0) {
         k_fold<<<1, 1024, 0, st>>>(r.L.partials, r.nblocks, r.L.red_op, red_dev_ + r.red);
         TCG_CK(cudaGetLastError());
         ++launches_;

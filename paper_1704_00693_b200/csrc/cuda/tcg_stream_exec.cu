@@ -115,6 +115,48 @@ void DeviceExec::launch_stream(void* fn, int64_t grid, int nt, int smem, const v
   ++launches_;
 }
 
+double* DeviceExec::slab_ptr(int f, int64_t s) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  const int d = b->alloc.dim() - 1;
+  if (s < b->alloc.start(d) || s > b->alloc.end(d)) throw AccessError("slab_ptr: slab outside the allocation");
+  const int64_t pitch = d == 2 ? b->pz : (d == 1 ? b->py : 1);
+  return b->mem[b->cur] + (s - b->alloc.start(d)) * pitch;
+}
+
+size_t DeviceExec::slab_count(int f, int64_t s0, int64_t s1) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  const int d = b->alloc.dim() - 1;
+  const int64_t pitch = d == 2 ? b->pz : (d == 1 ? b->py : 1);
+  return static_cast<size_t>(std::max<int64_t>(0, s1 - s0) * pitch);
+}
+
+bool DeviceExec::same_cross_section(int fa, int fb) const {
+  const Buf* a = fields_.at(static_cast<size_t>(fa));
+  const Buf* b = fields_.at(static_cast<size_t>(fb));
+  if (a->alloc.dim() != b->alloc.dim() || a->alloc.dim() < 2) return false;
+  for (int d = 0; d + 1 < a->alloc.dim(); ++d)
+    if (a->alloc.start(d) != b->alloc.start(d) || a->alloc.end(d) != b->alloc.end(d)) return false;
+  return a->x0 == b->x0 && a->py == b->py && a->pz == b->pz;
+}
+
+void DeviceExec::note_slab_write(int f, int64_t s0, int64_t s1) {
+  Buf* b = fields_.at(static_cast<size_t>(f));
+  Range box = b->alloc;
+  box.set_raw(b->alloc.dim() - 1, s0, s1);
+  mark_written(f, box);
+}
+
+void DeviceExec::copy_slabs(int f_dst, int f_src, int64_t s0, int64_t s1) {
+  if (s1 <= s0) return;
+  if (!same_cross_section(f_dst, f_src)) throw AccessError("copy_slabs: the fields differ in a faster dimension");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  // Rank r of a single-process multi-device run lives on device r % ndev;
+  // here both ranks share this executor's device, and the peer copy is a
+  // device-to-device copy.
+  TCG_CK(cudaMemcpyPeerAsync(slab_ptr(f_dst, s0), device_, slab_ptr(f_src, s0), device_, slab_count(f_src, s0, s1) * sizeof(double), st));
+  note_slab_write(f_dst, s0, s1);
+}
+
 void DeviceExec::read_device(double* host, const double* dev, size_t n) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   if (n > host_stage_n_) {

@@ -82,6 +82,21 @@ class DeviceExec {
   // Device staging for halo messages: >= n doubles, valid until the next
   // call that needs more.
   double* staging(size_t n);
+  // Contiguous slabs along the slowest dimension (whole rows in 2D, whole
+  // planes in 3D, pitch padding included): the halo messages of a domain
+  // split along that dimension need no packing.
+  //   slab_ptr   first element of slab coordinate s of field f
+  //   slab_count doubles in slabs [s0, s1)
+  //   same_cross_section  both fields share every faster dimension's range
+  //                       and pitch, so slab s of one maps onto slab s of the other
+  //   copy_slabs f_dst[s0, s1) <- f_src[s0, s1) (cudaMemcpyPeerAsync: the same
+  //              call carries a rank pair hosted on two devices of one process)
+  double* slab_ptr(int f, int64_t s);
+  size_t slab_count(int f, int64_t s0, int64_t s1);
+  bool same_cross_section(int fa, int fb) const;
+  void copy_slabs(int f_dst, int f_src, int64_t s0, int64_t s1);
+  void note_slab_write(int f, int64_t s0, int64_t s1);
+  int device_index() const { return device_; }
   // Device buffer for reduction partials exchanged between processes.
   double* red_buffer(size_t n);
   // Stream-ordered small copies; d2h synchronizes the stream.
@@ -159,6 +174,13 @@ class DeviceExec {
   double* st_out_ = nullptr;
   size_t st_out_n_ = 0;
   unsigned* st_ticket_ = nullptr;
+  int device_ = 0;
+  // Order-matched Sum reductions (set_reduction_workers).
+  int red_workers_ = 0;
+  double* capture_ = nullptr;
+  size_t capture_n_ = 0;
+  double* ord_part_ = nullptr;
+  unsigned* ord_ticket_ = nullptr;
   double* host_stage_ = nullptr;  // pinned
   size_t host_stage_n_ = 0;
   double* red_host_ = nullptr;  // pinned
@@ -187,6 +209,14 @@ class DeviceExec {
   void* take_event();
   void* ensure_scratch(size_t bytes);
   double* ensure_partials(size_t n);
+ public:
+  // Sum reductions of untiled chains folded in the reference's order for a
+  // pool of `workers` threads (executor.cpp:55-61, :141-144, :175-176):
+  // sequential sums over the static memory-order spans, then a worker-order
+  // fold. 0 (default): warp/block tree fold. At most 1024 workers.
+  void set_reduction_workers(int workers) { red_workers_ = workers < 0 ? 0 : (workers > 1024 ? 1024 : workers); }
+  int reduction_workers() const { return red_workers_; }
+ private:
   void ensure_red(size_t n);
   PlanBufs* plan_bufs(const GpuTiledPlan& gp, uint64_t key);
 };

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 
 #include "../kernels/tc_bodies.h"
@@ -142,7 +143,7 @@ std::string ExecutionReport::to_text() const {
   std::snprintf(b, sizeof b, "%.6f", total_seconds);
   kv("total_seconds", b);
   kv("launches", std::to_string(launches));
-  if (distributed) {
+  if (distributed || halo_exchanges > 0) {
     kv("halo_messages", std::to_string(halo_messages));
     kv("halo_bytes", std::to_string(halo_bytes));
     kv("halo_exchanges", std::to_string(halo_exchanges));
@@ -282,7 +283,11 @@ ReductionHandle Runtime::par_loop(KernelHandle kernel, const Range& range, std::
     mix(kernel.fn.params.size());
     for (const ArgSpec& a : args) mix((static_cast<uint64_t>(a.stencil) << 8) | static_cast<uint64_t>(a.mode));
     mix(stencils_.size());
-    if (!body_sig_ok_.count(key)) {
+    static const bool skip_probe = [] {
+      const char* e = std::getenv("TCG_SKIP_BODY_PROBE");  // test hook: lets the checked device build see the fault
+      return e && *e == '1';
+    }();
+    if (!skip_probe && !body_sig_ok_.count(key)) {
       if (args.empty()) throw InvalidArgument("par_loop: kernel " + kernel.name + " declares no arguments");
       ProbeAcc probe{args, stencils_, reduction.has_value(), {}};
       std::vector<double> prm(kernel.fn.params.begin(), kernel.fn.params.end());
@@ -315,6 +320,13 @@ ReductionHandle Runtime::par_loop(KernelHandle kernel, const Range& range, std::
   }
   pending_.push_back(std::move(rec));
   return h;
+}
+
+void Runtime::set_reduction_order(int workers) {
+  if (workers < 0 || workers > 1024) throw InvalidArgument("set_reduction_order: workers must be in [0, 1024]");
+  flush();
+  red_workers_ = workers;
+  if (dev_) dev_->set_reduction_workers(workers);
 }
 
 void Runtime::record_begin() {
@@ -931,7 +943,14 @@ std::vector<double> Runtime::run_on(const LoopChain& full, const ExecMode& mode,
                                                      : 0;
   AutoStat* as = nullptr;
   bool measure = false;
-  if (mode.kind == ExecMode::Kind::TiledAuto) {
+  bool sum_ordered = false;
+  if (red_workers_ > 0)
+    for (const LoopRecord& lp : chain.loops) sum_ordered = sum_ordered || (lp.reduction && lp.reduction->op == ReduceOp::Sum);
+  if (sum_ordered) {
+    if (t.masked) throw InvalidArgument("order-matched Sum reductions are not available on a rank grid");
+    dev.set_reduction_workers(red_workers_);
+    cand = 1;  // the reference order is the untiled executor's (execute_untiled, executor.cpp:252-277)
+  } else if (mode.kind == ExecMode::Kind::TiledAuto) {
     const uint64_t akey = chain.signature() ^ mask_hash(*this, t.masked, t.mask, chain.dim);
     auto ait = auto_.find(akey);
     if (ait == auto_.end()) {
@@ -1045,6 +1064,11 @@ std::vector<StreamGeom> Runtime::stream_geoms(const Target& t, bool from_device)
 
 StreamPlan Runtime::stream_plan_pending(const StreamDevice& sd) {
   LoopChain chain = take_pending();
+  if (!chain.fills.empty()) {
+    std::vector<Range> logical;
+    for (const FieldRec& f : fields_) logical.push_back(f.logical);
+    chain = apply_periodic(chain, logical).chain;
+  }
   Target t;
   for (const FieldRec& f : fields_) {
     t.dev.push_back(-1);
@@ -1396,24 +1420,50 @@ void Runtime::exchange(const DistSchedule& s, ExecutionReport& rep) {
   DeviceExec& dev = device();
   std::vector<char> is_local(static_cast<size_t>(dist_->layout.rank_count()), 0);
   for (int r : dist_->local) is_local[static_cast<size_t>(r)] = 1;
+  static const bool direct_ok = [] {
+    const char* e = std::getenv("TCG_HALO_DIRECT");
+    return !(e && *e == '0');
+  }();
+  // A message along the slowest dimension between ranks that share every
+  // faster dimension's allocation (a z-split in 3D, a y-split in 2D) is a run
+  // of whole planes / rows: contiguous in both fields, so it moves straight
+  // from field to field -- a peer copy inside this process, ncclSend/ncclRecv
+  // on the field memory between processes -- with no staging pack (the
+  // reference's message, dist.cpp:463-511, widened to whole slabs: the extra
+  // points are pad columns of the same slabs). The message log keeps the
+  // reference's box geometry.
+  auto direct = [&](const HaloMsg& m, int d) {
+    if (!direct_ok || d != dim_ - 1 || dim_ < 2) return false;
+    const Range as = rank_alloc(dist_->layout, m.src, fields_[static_cast<size_t>(m.ds)].pad);
+    const Range ad = rank_alloc(dist_->layout, m.dst, fields_[static_cast<size_t>(m.ds)].pad);
+    for (int e = 0; e + 1 < dim_; ++e)
+      if (as.start(e) != ad.start(e) || as.end(e) != ad.end(e)) return false;
+    const bool ls = is_local[static_cast<size_t>(m.src)], ld = is_local[static_cast<size_t>(m.dst)];
+    if (ls && ld)
+      return dev.same_cross_section(dist_->targets[static_cast<size_t>(m.dst)].dev[static_cast<size_t>(m.ds)],
+                                    dist_->targets[static_cast<size_t>(m.src)].dev[static_cast<size_t>(m.ds)]);
+    return true;  // remote peer: same declaration, same layout rule
+  };
   for (int d = 0; d < kMaxDims; ++d) {
     const size_t a = s.phase[static_cast<size_t>(d)], b = s.phase[static_cast<size_t>(d) + 1];
     if (a == b) continue;
-    // Staging offsets of the messages this process takes part in.
+    // Staging offsets of the packed messages this process takes part in.
     std::vector<size_t> off(b - a, 0);
+    std::vector<char> dir(b - a, 0);
     size_t total = 0;
     for (size_t i = a; i < b; ++i) {
       const HaloMsg& m = s.msgs[i];
       if (!is_local[static_cast<size_t>(m.src)] && !is_local[static_cast<size_t>(m.dst)]) continue;
+      dir[i - a] = direct(m, d) ? 1 : 0;
+      if (dir[i - a]) continue;
       off[i - a] = total;
       total += static_cast<size_t>(m.points);
     }
-    if (total == 0) continue;
-    double* stg = dev.staging(total);
-    // Pack every message whose source rank lives here.
+    double* stg = total ? dev.staging(total) : nullptr;
+    // Pack every staged message whose source rank lives here.
     for (size_t i = a; i < b; ++i) {
       const HaloMsg& m = s.msgs[i];
-      if (!is_local[static_cast<size_t>(m.src)]) continue;
+      if (dir[i - a] || !is_local[static_cast<size_t>(m.src)]) continue;
       const Target& t = dist_->targets[static_cast<size_t>(m.src)];
       dev.field_to_buf(t.dev[static_cast<size_t>(m.ds)], m.box, stg + off[i - a], m.box);
     }
@@ -1427,17 +1477,39 @@ void Runtime::exchange(const DistSchedule& s, ExecutionReport& rep) {
         for (size_t i = a; i < b; ++i) {
           const HaloMsg& m = s.msgs[i];
           const bool ls = is_local[static_cast<size_t>(m.src)], ld = is_local[static_cast<size_t>(m.dst)];
-          if (ls && !ld) comm_->send(stg + off[i - a], static_cast<size_t>(m.points), m.dst, dev.stream());
-          if (ld && !ls) comm_->recv(stg + off[i - a], static_cast<size_t>(m.points), m.src, dev.stream());
+          if (ls == ld) continue;
+          const int64_t s0 = m.box.start(dim_ - 1), s1 = m.box.end(dim_ - 1);
+          if (ls) {
+            const int f = dist_->targets[static_cast<size_t>(m.src)].dev[static_cast<size_t>(m.ds)];
+            if (dir[i - a])
+              comm_->send(dev.slab_ptr(f, s0), dev.slab_count(f, s0, s1), m.dst, dev.stream());
+            else
+              comm_->send(stg + off[i - a], static_cast<size_t>(m.points), m.dst, dev.stream());
+          } else {
+            const int f = dist_->targets[static_cast<size_t>(m.dst)].dev[static_cast<size_t>(m.ds)];
+            if (dir[i - a]) {
+              comm_->recv(dev.slab_ptr(f, s0), dev.slab_count(f, s0, s1), m.src, dev.stream());
+              dev.note_slab_write(f, s0, s1);
+            } else {
+              comm_->recv(stg + off[i - a], static_cast<size_t>(m.points), m.src, dev.stream());
+            }
+          }
         }
         comm_->group_end();
       }
     }
-    // Unpack every message whose destination rank lives here.
+    // Local pairs: direct slab copies; staged messages unpack at their destination.
     for (size_t i = a; i < b; ++i) {
       const HaloMsg& m = s.msgs[i];
       if (!is_local[static_cast<size_t>(m.dst)]) continue;
       const Target& t = dist_->targets[static_cast<size_t>(m.dst)];
+      if (dir[i - a]) {
+        if (is_local[static_cast<size_t>(m.src)])
+          dev.copy_slabs(t.dev[static_cast<size_t>(m.ds)],
+                         dist_->targets[static_cast<size_t>(m.src)].dev[static_cast<size_t>(m.ds)],
+                         m.box.start(dim_ - 1), m.box.end(dim_ - 1));
+        continue;
+      }
       dev.buf_to_field(t.dev[static_cast<size_t>(m.ds)], m.box, stg + off[i - a], m.box);
     }
   }

@@ -114,6 +114,14 @@ class Runtime {
   // false (default): it records a PeriodicMark in the queue and the chain is
   // rewritten at flush (tcg_periodic.hpp) -- one wrap per chain.
   void set_periodic_flush(bool v) { periodic_flush_ = v; }
+  // Order-matched Sum reductions: chains with a Sum reduction run on the
+  // untiled executor and fold in the reference's order for a pool of
+  // `workers` threads (executor.cpp:55-61 static spans, :141-144 sequential
+  // per-worker partials, :175-176 worker-order fold), so a c4 residual
+  // history follows RefRuntime(threads = workers, untiled) bit for bit.
+  // 0 (default): the fast tree fold.
+  void set_reduction_order(int workers);
+  int reduction_order() const { return red_workers_; }
   // Bulk host <-> device copies of a whole allocation (dense, dim 0 fastest,
   // the reference Field layout, field.cpp:22-26). Flush first.
   void upload(DatasetId ds, const double* host);
@@ -254,6 +262,7 @@ class Runtime {
   std::vector<RecordedCall> record_cur_;
   std::vector<std::vector<RecordedCall>> recorded_;
   bool periodic_flush_ = false;
+  int red_workers_ = 0;
   std::unordered_set<uint64_t> body_sig_ok_;  // (body, declaration) pairs the probe accepted
   ExecMode default_mode_;
   std::vector<Slot> slots_;

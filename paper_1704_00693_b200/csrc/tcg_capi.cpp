@@ -373,6 +373,9 @@ int tcg_local_box(tcg_runtime* rt, int32_t ds, int64_t out[6]) {
   });
 }
 
+int tcg_set_reduction_order(tcg_runtime* rt, int workers) {
+  return guard([&] { rt->rt->set_reduction_order(workers); });
+}
 int tcg_record_begin(tcg_runtime* rt) {
   return guard([&] { rt->rt->record_begin(); });
 }

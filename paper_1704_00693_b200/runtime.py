@@ -108,6 +108,7 @@ def load_library() -> ctypes.CDLL:
         "tcg_set_rank_grid": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
         "tcg_periodic_fill": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I32), _I64]),
         "tcg_set_periodic_flush": (ctypes.c_int, [_P, ctypes.c_int]),
+        "tcg_set_reduction_order": (ctypes.c_int, [_P, ctypes.c_int]),
         "tcg_record_begin": (ctypes.c_int, [_P]),
         "tcg_record_end": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
         "tcg_replay": (ctypes.c_int, [_P, _I32, ctypes.POINTER(ctypes.c_double), _I64, ctypes.POINTER(_I32), _I64,
@@ -530,6 +531,11 @@ class Runtime:
     def periodic_plan_pending(self) -> str:
         """Host-only: the pending chain rewritten around its periodic marks."""
         return _text(self._lib.tcg_periodic_plan_pending, self._h)
+
+    def set_reduction_order(self, workers: int) -> None:
+        """Fold Sum reductions in the reference's order for `workers` threads
+        (untiled executor, sequential span sums, worker-order fold); 0 = fast."""
+        _check(self._lib.tcg_set_reduction_order(self._h, workers))
 
     # ---- step templates ------------------------------------------------------
     def record_begin(self) -> None:

@@ -36,6 +36,10 @@ SIZES = {
     "c2": {"n": 4096, "steps": 50},
     "c3": {"n": 512, "chains": 5},       # 40 sweeps, 8 per 16-loop chain
     "c4": {"n": 4096, "iters": 140},     # the self-consistent window of the 200-iteration run
+    # The whole BASELINE history: compared against the product's order-matched
+    # Sum mode (Runtime.set_reduction_order(threads)), which reproduces the
+    # reference's worker fold, so all 200 iterations must agree.
+    "c4_ordered": {"n": 4096, "iters": 200, "threads": 8},
 }
 
 
@@ -62,7 +66,7 @@ def run(name: str, rt, size: dict):
             c.enqueue_chain()
             rt.flush()
         return c.outputs(), []
-    if name == "c4":
+    if name in ("c4", "c4_ordered"):
         c = configs.CgC4(rt, size["n"])
         c.start()
         for _ in range(size["iters"]):
@@ -79,6 +83,7 @@ def main(argv):
     for name in names:
         size = SIZES[name]
         t0 = time.time()
+        threads = size.get("threads", os.cpu_count() or 1)
         rt = po.RefRuntime(3 if name == "c3" else 2, threads=threads)
         rt.set_default_mode(ExecMode.untiled())
         fields, hist = run(name, rt, size)

@@ -24,6 +24,7 @@ sys.path.insert(0, {repo!r}); sys.path.insert(0, {repo!r} + "/oracle")
 import numpy as np
 import pyoracle
 from paper_1704_00693_b200 import AccessMode, ArgSpec, CudaError, ExecMode, KernelHandle, Range, Runtime, configs
+from paper_1704_00693_b200.runtime import AccessError
 from paper_1704_00693_b200 import kernels as K
 """
 
@@ -79,11 +80,13 @@ try:
     print("device did not trap")
 except CudaError as e:
     print("device trapped")
+except AccessError as e:
+    print("enqueue refused:", e)
 """
 
 
-def _child(code):
-    env = {**os.environ, "TCG_LIB": str(LIB)}
+def _child(code, **extra):
+    env = {**os.environ, "TCG_LIB": str(LIB), **extra}
     return subprocess.run([sys.executable, "-c", code.format(repo=str(REPO))], env=env, capture_output=True,
                           text=True, timeout=600)
 
@@ -95,8 +98,18 @@ def test_checked_build_runs_correct_chains_bit_exact():
 
 
 def test_checked_build_traps_read_outside_stencil():
-    r = _child(BAD)
+    # With the host probe of par_loop switched off (test hook) the fault
+    # reaches the device, where the checked build reports and traps it.
+    r = _child(BAD, TCG_SKIP_BODY_PROBE="1")
     out = r.stdout + r.stderr
     assert "oracle raised: offset not in declared stencil" in r.stdout, out[-4000:]
     assert "device trapped" in r.stdout, out[-4000:]
     assert "offset is not a point of the argument's stencil" in out, out[-4000:]
+
+
+def test_enqueue_refuses_read_outside_stencil():
+    # Default: par_loop's host probe of the registered body raises the
+    # reference's AccessError before anything is queued (kernel_ctx.hpp:58-73).
+    r = _child(BAD)
+    out = r.stdout + r.stderr
+    assert "enqueue refused:" in r.stdout and "offset not in declared stencil" in r.stdout, out[-4000:]

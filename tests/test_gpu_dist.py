@@ -177,3 +177,92 @@ def test_poisoned_stale_halos_stay_exact(oracle_lib, monkeypatch, mode, seed, di
         al = rt.alloc_range(d)
         sl = tuple(slice(lg.start(k) - al.start(k), lg.end(k) - al.start(k)) for k in reversed(range(dim)))
         assert np.array_equal(g[sl], w[sl]), d
+
+
+_TWO_RANK = r"""
+import os, sys
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {repo!r} + "/tests")
+import numpy as np
+import torch, torch.distributed as dist
+rank = int(os.environ["RANK"]); world = int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+import paper_1704_00693_b200 as pkg
+from paper_1704_00693_b200 import ExecMode, Runtime, configs
+pkg.runtime.select_device(rank)
+obj = [pkg.comm_unique_id() if rank == 0 else None]
+dist.broadcast_object_list(obj, src=0)
+rt = Runtime(3)
+rt.set_process_rank((1, 1, world), rank, obj[0])
+rt.set_default_mode(ExecMode.{mode}())
+c = configs.Jacobi3DC3(rt, 48)
+for _ in range(2):
+    c.enqueue_chain()
+    rt.flush()
+box = rt.local_box(c.a)
+mine = rt.download_box(c.a, box)
+ref = Runtime(3)
+ref.set_default_mode(ExecMode.untiled())
+cr = configs.Jacobi3DC3(ref, 48)
+for _ in range(2):
+    cr.enqueue_chain()
+    ref.flush()
+want = ref.download_box(cr.a, box)
+# compare the planes this rank owns
+z0 = box.start(2); n = 48 // world
+lo = rank * n - z0; hi = lo + n
+assert np.array_equal(mine[lo:hi], want[lo:hi]), "rank %d differs" % rank
+print("rank", rank, "ok", flush=True)
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("mode", ["tiled_auto", "untiled"])
+def test_two_process_nccl_z_split(tmp_path, mode):
+    # One rank per process / GPU, the deep-halo exchange carried by
+    # ncclSend/ncclRecv straight from the field slabs. Needs two GPUs.
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import subprocess, sys, os
+    from pathlib import Path
+    repo = str(Path(__file__).resolve().parent.parent)
+    script = tmp_path / "two_rank.py"
+    script.write_text(_TWO_RANK.format(repo=repo, mode=mode))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29541", str(script)],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.count(" ok") == 2, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_depth_guard_refuses_halo_deeper_than_neighbour():
+    # c3-shaped chain at N = 32 over 4 z-ranks: the 16-loop chain's halo depth
+    # exceeds a neighbour's owned width (8 planes); the reference would read
+    # stale values there (SURVEY.md §4), the schedule builder refuses.
+    from paper_1704_00693_b200.runtime import PlanError
+    rt = _GridRuntime(3, (1, 1, 4))
+    rt.set_default_mode(ExecMode.tiled((0, 0, 0)))
+    c = configs.Jacobi3DC3(rt, 32)
+    c.enqueue_chain()
+    with pytest.raises(PlanError):
+        rt.flush()
+
+
+@pytest.mark.parametrize("mode", [ExecMode.tiled_auto(), ExecMode.stream(), ExecMode.untiled()],
+                         ids=["auto", "stream", "untiled"])
+def test_c3_z_split_simulated_ranks_use_slab_copies(oracle_lib, mode):
+    # BASELINE c3's decomposition (along z) on simulated ranks: the halo
+    # messages are whole planes and move field to field (copy_slabs, the
+    # peer-copy path), no staging pack.
+    ort = oracle_lib.OracleRuntime(3)
+    co = configs.Jacobi3DC3(ort, 40)
+    rt = _GridRuntime(3, (1, 1, 2))
+    rt.set_default_mode(mode)
+    cg = configs.Jacobi3DC3(rt, 40)
+    for _ in range(2):
+        co.enqueue_chain()
+        ort.flush()
+        cg.enqueue_chain()
+        rt.flush()
+    rep = parse_report(rt.report_text())
+    assert int(rep["halo_messages"]) > 0
+    assert np.array_equal(cg.outputs()["a"], co.outputs()["a"])

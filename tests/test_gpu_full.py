@@ -61,3 +61,41 @@ def test_full_size_cg_history_matches_reference(mode):
     assert got.shape == want.shape
     rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-300)
     assert rel.max() <= 1e-10, (int(rel.argmax()), float(rel.max()))
+
+
+def test_full_size_cg_order_matched_history_follows_reference_for_all_iterations():
+    # Order-matched Sum mode (SURVEY.md §7 Option A): sequential sums over the
+    # reference's static spans for T workers, worker-order fold
+    # (executor.cpp:55-61, :141-144, :175-176). The whole 200-iteration
+    # BASELINE history then follows the untiled reference with T threads --
+    # past iteration ~140, where fold orders otherwise diverge.
+    want = GOLD["c4_ordered"]
+    rt = Runtime(2)
+    rt.set_reduction_order(want["threads"])
+    rt.set_default_mode(ExecMode.tiled_auto())  # Sum chains run untiled whatever the mode
+    _, hist = G.run("c4_ordered", rt, want["size"])
+    ref = np.array([float.fromhex(x) for x in want["history"]])
+    got = np.array(hist)
+    assert got.shape == ref.shape == (201,)
+    rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)
+    assert rel.max() <= 1e-10, (int(rel.argmax()), float(rel.max()))
+    assert [float(x).hex() for x in hist] == want["history"]  # in fact bit for bit
+
+
+def test_order_matched_sum_small_matches_reference_threads(ref_lib):
+    # Small case against the live reference library at several thread counts.
+    import pyoracle as po
+    from paper_1704_00693_b200 import configs
+    for threads in (1, 3, 8):
+        rr = po.RefRuntime(2, threads=threads)
+        rr.set_default_mode(ExecMode.untiled())
+        cr = configs.CgC4(rr, 96)
+        cr.start()
+        rt = Runtime(2)
+        rt.set_reduction_order(threads)
+        cg = configs.CgC4(rt, 96)
+        cg.start()
+        for _ in range(25):
+            cr.iterate()
+            cg.iterate()
+        assert [float(x).hex() for x in cg.history] == [float(x).hex() for x in cr.history], threads

@@ -2,7 +2,7 @@
 # GPU parity suite + default stream/untiled/auto bench lines per config.
 cd "$GRAFT_REPO_ROOT"; OUT=gpurun_out/${TAG:-gc}; mkdir -p $OUT
 export TCG_JIT_CACHE=/tmp/tcg_jit
-timeout ${TEST_TIMEOUT:-1500} python -m pytest tests -m gpu -q -x ${PYTEST_ARGS} > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $OUT/pytest_gpu.log
+timeout ${TEST_TIMEOUT:-1500} python -m pytest tests -m gpu -q ${PYTEST_ARGS} > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $OUT/pytest_gpu.log
 for c in ${CONFIGS:-c2 c3 c1}; do
   for m in ${MODES:-stream untiled auto}; do
     timeout 400 python bench.py --config $c --mode $m --steps ${STEPS:-20} --warmup 10 --no-cpu-baseline --no-e2e --no-untiled > $OUT/bench_${c}_$m.json 2> $OUT/bench_${c}_$m.err
