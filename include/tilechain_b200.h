@@ -135,6 +135,11 @@ int tcg_fill_logical(tcg_runtime* rt, int32_t ds, double v);
  * form: flush, then copy the opposite side into the ghost layers. */
 int tcg_periodic_fill(tcg_runtime* rt, int n, const int32_t* ds, int64_t depth);
 int tcg_set_periodic_flush(tcg_runtime* rt, int flush_each);
+/* Periodic box on a rank grid (before tcg_set_rank_grid / tcg_set_process_rank):
+ * the ghost layers join the decomposed domain (owned by the end ranks) and the
+ * wrap along the split (slowest) dimension is one slab message between the
+ * end ranks per chain -- a self-exchange at one rank. */
+int tcg_set_periodic_domain(tcg_runtime* rt, int on);
 /* Host-only: the rewrite of the pending chain around its periodic marks
  * (extended loop ranges, datasets wrapped before the chain); consumed. */
 int tcg_periodic_plan_pending(tcg_runtime* rt, char* buf, int64_t n, int64_t* needed);

@@ -85,6 +85,7 @@ def load_ref():
             "tcref_plan_pending": [_P, _P, ctypes.c_char_p, _I64],
             "tcref_validate_plan": [_P, _P, _P, _I64, ctypes.c_int, ctypes.c_char_p, _I64],
             "tcref_rank_plans_pending": [_P, _P, _P, ctypes.c_char_p, _I64],
+            "tcref_validate_rank_plans": [_P, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, ctypes.c_char_p, _I64],
             "tcref_dist_info": [_P, ctypes.c_char_p, _I64],
             "tcref_auto_tile_size": [ctypes.c_int, _I64, ctypes.c_int, _I64, _P, _P],
             "tcref_app_jacobi": [_I64, _I64, ctypes.c_int, ctypes.c_int, _P],
@@ -288,6 +289,19 @@ class RefRuntime(_Base):
         buf = ctypes.create_string_buffer(1 << 20)
         n = self.lib.tcref_validate_plan(self.h, _arr(_I64, ts[:3]), _arr(_I64, ranges), ntiles, nloops, buf,
                                          len(buf))
+        if n < 0:
+            raise OracleError(self.lib.tcref_error().decode())
+        return int(n), buf.value.decode()
+
+    def validate_rank_plans_pending(self, nranks, nloops, ranges, owned, band, skip):
+        """The reference's validate_dependencies (per rank) and
+        validate_coverage_replicated (over the owned parts) on overlapped
+        single-tile plans -- the streaming executor's CTA plans. Consumes the
+        pending chain. Returns (violations, text)."""
+        buf = ctypes.create_string_buffer(1 << 20)
+        band = list(band) + [0] * (3 - len(band))
+        n = self.lib.tcref_validate_rank_plans(self.h, nranks, nloops, _arr(_I64, ranges), _arr(_I64, owned),
+                                               _arr(_I64, band[:3]), _arr(_I32, skip), buf, len(buf))
         if n < 0:
             raise OracleError(self.lib.tcref_error().decode())
         return int(n), buf.value.decode()

@@ -315,6 +315,69 @@ int64_t tcref_validate_plan(void* hv, const int64_t* ts3, const int64_t* ranges,
   return rc < 0 ? rc : count;
 }
 
+// Consumes the pending queue: the reference's validators applied to a set of
+// overlapped single-tile plans -- one per "rank", here one per CTA of the
+// streaming executor (a CTA recomputes its halo like a rank of
+// construct_rank_plan, dist.cpp:268-310). ranges[(r*L + l)*6 ...] is the box
+// rank r computes of loop l (empty = not executed), owned[r*6 ...] its owned
+// box, band[d] the replication band allowed around the owned cuts, skip[l] != 0
+// marks loops the executor drops (their output is dead).
+//   * validate_dependencies (oracle.cpp:154-223) per rank: every point a rank
+//     reads must have been produced, inside the same rank, by the loop that
+//     produces it in sequential order (nothing may come from a neighbour);
+//   * validate_coverage_replicated (oracle.cpp:286-344) over the owned parts:
+//     every recorded point owned exactly once.
+// Returns the number of violations; text to buf.
+int64_t tcref_validate_rank_plans(void* hv, int32_t nranks, int32_t nloops, const int64_t* ranges, const int64_t* owned,
+                                  const int64_t* band3, const int32_t* skip, char* buf, int64_t n) {
+  auto* h = static_cast<Handle*>(hv);
+  int64_t count = -1;
+  const int64_t rc = guarded([&]() -> int64_t {
+    LoopChain chain = h->rt->take_pending();
+    if (static_cast<int32_t>(chain.size()) != nloops) throw InvalidArgument("validate_rank_plans: loop count differs");
+    const int64_t big = int64_t{1} << 40;
+    PlanConfig cfg = compute_union_bounds(chain, {big, big, big});
+    if (cfg.total_tiles() != 1) throw InvalidArgument("validate_rank_plans: expected a single-tile grid");
+    auto box = [&](const int64_t* p) {
+      Range r(chain.dim);
+      for (int d = 0; d < chain.dim; ++d) r.set(d, p[2 * d], std::max(p[2 * d], p[2 * d + 1]));
+      return r;
+    };
+    std::vector<oracle::Violation> v;
+    std::vector<TilingPlan> exec_plans, own_plans;
+    std::vector<Range> own;
+    for (int32_t r = 0; r < nranks; ++r) {
+      std::vector<Range> rs, os;
+      const Range ob = box(owned + static_cast<size_t>(r) * 6);
+      own.push_back(ob);
+      for (int32_t l = 0; l < nloops; ++l) {
+        const Range x = box(ranges + (static_cast<size_t>(r) * nloops + l) * 6);
+        rs.push_back(x);
+        os.push_back(skip[l] ? x : x.intersect(ob));
+      }
+      exec_plans.emplace_back(cfg, chain.signature(), nloops, std::move(rs), DependencyExtents{}, 0.0);
+      own_plans.emplace_back(cfg, chain.signature(), nloops, std::move(os), DependencyExtents{}, 0.0);
+    }
+    for (int32_t r = 0; r < nranks && v.size() < 32; ++r)
+      for (oracle::Violation& x : oracle::validate_dependencies(exec_plans[static_cast<size_t>(r)], chain, 8)) {
+        x.detail += " [rank " + std::to_string(r) + "]";
+        v.push_back(x);
+      }
+    std::vector<const TilingPlan*> ptrs;
+    for (const TilingPlan& p : own_plans) ptrs.push_back(&p);
+    for (const oracle::Violation& x :
+         oracle::validate_coverage_replicated(ptrs, chain, own, {band3[0], band3[1], band3[2]}, 32)) {
+      if (x.loop >= 0 && x.loop < nloops && skip[x.loop]) continue;
+      v.push_back(x);
+    }
+    std::ostringstream os;
+    for (const oracle::Violation& x : v) os << x.to_string() << "\n";
+    count = static_cast<int64_t>(v.size());
+    return put_text(os.str(), buf, n);
+  });
+  return rc < 0 ? rc : count;
+}
+
 // Consumes the pending queue; per rank of decompose(global, grid):
 // construct_rank_plan (dist.cpp:191-390) + compute_halo_depths (:407-448).
 int64_t tcref_rank_plans_pending(void* hv, const int* g3, const int64_t* ts3, char* buf, int64_t n) {

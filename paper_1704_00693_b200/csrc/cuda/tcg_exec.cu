@@ -880,9 +880,10 @@ void DeviceExec::copy_within(int f, const Range& box, const Point& shift) {
   mark_written(f, box);
 }
 
-void DeviceExec::periodic_fill(const std::vector<int>& fields, const Range& logical, int64_t depth) {
+void DeviceExec::periodic_fill(const std::vector<int>& fields, const Range& logical, int64_t depth, int ndims) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   const int dim = logical.dim();
+  const int nd = ndims < 0 ? dim : std::min(ndims, dim);
   for (size_t b = 0; b < fields.size(); b += kMaxPeriodic) {
     PLaunch P{};
     P.nf = static_cast<int32_t>(std::min<size_t>(kMaxPeriodic, fields.size() - b));
@@ -895,7 +896,7 @@ void DeviceExec::periodic_fill(const std::vector<int>& fields, const Range& logi
       const DevView v = view(fields[b + static_cast<size_t>(k)], false);
       P.f[k] = UArg{v.base, v.x0, v.y0, v.z0, v.py, v.pz, 0, 0};
     }
-    for (int d = 0; d < dim; ++d) {
+    for (int d = 0; d < nd; ++d) {
       int64_t total = 2 * depth;
       for (int e = 0; e < dim; ++e)
         if (e != d) total *= (logical.extent(e) + (e < d ? 2 * depth : 0));
@@ -914,7 +915,7 @@ void DeviceExec::periodic_fill(const std::vector<int>& fields, const Range& logi
   // Ghost layers written: the slabs outside the logical box, every dimension.
   for (int f : fields) {
     const Range& al = fields_.at(static_cast<size_t>(f))->alloc;
-    for (int d = 0; d < dim; ++d)
+    for (int d = 0; d < nd; ++d)
       for (int side = 0; side < 2; ++side) {
         Range g(dim);
         for (int e = 0; e < dim; ++e) {

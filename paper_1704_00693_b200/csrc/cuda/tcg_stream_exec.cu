@@ -136,7 +136,7 @@ bool DeviceExec::same_cross_section(int fa, int fb) const {
   if (a->alloc.dim() != b->alloc.dim() || a->alloc.dim() < 2) return false;
   for (int d = 0; d + 1 < a->alloc.dim(); ++d)
     if (a->alloc.start(d) != b->alloc.start(d) || a->alloc.end(d) != b->alloc.end(d)) return false;
-  return a->x0 == b->x0 && a->py == b->py && a->pz == b->pz;
+  return a->x0 == b->x0 && a->py == b->py && (a->alloc.dim() < 3 || a->pz == b->pz);
 }
 
 void DeviceExec::note_slab_write(int f, int64_t s0, int64_t s1) {
@@ -155,6 +155,15 @@ void DeviceExec::copy_slabs(int f_dst, int f_src, int64_t s0, int64_t s1) {
   // device-to-device copy.
   TCG_CK(cudaMemcpyPeerAsync(slab_ptr(f_dst, s0), device_, slab_ptr(f_src, s0), device_, slab_count(f_src, s0, s1) * sizeof(double), st));
   note_slab_write(f_dst, s0, s1);
+}
+
+void DeviceExec::copy_slabs_shift(int f_dst, int64_t dst_s0, int f_src, int64_t src_s0, int64_t n) {
+  if (n <= 0) return;
+  if (!same_cross_section(f_dst, f_src)) throw AccessError("copy_slabs_shift: the fields differ in a faster dimension");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  TCG_CK(cudaMemcpyPeerAsync(slab_ptr(f_dst, dst_s0), device_, slab_ptr(f_src, src_s0), device_,
+                             slab_count(f_src, src_s0, src_s0 + n) * sizeof(double), st));
+  note_slab_write(f_dst, dst_s0, dst_s0 + n);
 }
 
 void DeviceExec::read_device(double* host, const double* dev, size_t n) {

@@ -78,7 +78,10 @@ class DeviceExec {
   void fill_box_bytes(int f, const Range& box, int byte);
   // Periodic ghost fill of fields (all with the same logical box), all
   // dimensions in order (edges/corners wrap), one kernel launch per dimension.
-  void periodic_fill(const std::vector<int>& fields, const Range& logical, int64_t depth);
+  // ndims >= 0: wrap only dimensions [0, ndims) (a rank of a grid split along
+  // the slowest dimension wraps the faster ones itself; the slowest one is
+  // carried between the end ranks as whole slabs).
+  void periodic_fill(const std::vector<int>& fields, const Range& logical, int64_t depth, int ndims = -1);
   // Device staging for halo messages: >= n doubles, valid until the next
   // call that needs more.
   double* staging(size_t n);
@@ -95,6 +98,8 @@ class DeviceExec {
   size_t slab_count(int f, int64_t s0, int64_t s1);
   bool same_cross_section(int fa, int fb) const;
   void copy_slabs(int f_dst, int f_src, int64_t s0, int64_t s1);
+  // f_dst[dst_s0, dst_s0 + n) <- f_src[src_s0, src_s0 + n): the periodic wrap along the slowest dimension.
+  void copy_slabs_shift(int f_dst, int64_t dst_s0, int f_src, int64_t src_s0, int64_t n);
   void note_slab_write(int f, int64_t s0, int64_t s1);
   int device_index() const { return device_; }
   // Device buffer for reduction partials exchanged between processes.

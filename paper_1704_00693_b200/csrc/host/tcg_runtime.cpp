@@ -329,6 +329,12 @@ void Runtime::set_reduction_order(int workers) {
   if (dev_) dev_->set_reduction_workers(workers);
 }
 
+void Runtime::set_periodic_domain(bool v) {
+  flush();
+  if (dist_) throw InvalidArgument("set_periodic_domain: call before the first distributed flush");
+  periodic_domain_ = v;
+}
+
 void Runtime::record_begin() {
   recording_ = true;
   record_cur_.clear();
@@ -1108,8 +1114,32 @@ void Runtime::run_stream(const LoopChain& chain, ExecutionReport& rep, const Tar
   for (const StreamKernel& k : plan.kernels) nred_total += k.red_op.size();
   std::vector<uint64_t> buf;
   size_t red_base = 0;
+  // Sub-chains of one loop have nothing to fuse: they run on the untiled
+  // executor (a single streamed loop costs about twice the untiled launch,
+  // measured on c3's 16th loop: 0.98 vs 0.47 ms; profiles/r5/sweeps.md).
+  static const bool singleton_untiled = [] {
+    const char* e = std::getenv("TCG_STREAM_SINGLETON_UNTILED");
+    return !(e && *e == '0');
+  }();
+  std::vector<double> host_vals(nred_total, 0.0);
+  std::vector<char> host_known(nred_total, 0);
   for (const StreamKernel& K : plan.kernels) {
     if (K.nctas == 0) continue;
+    const bool sized = stream_choice_.nt == 0 && stream_choice_.bx == 0 && stream_choice_.max_loops == 0;  // sizer's plan
+    if (singleton_untiled && sized && K.end - K.begin == 1 && plan.kernels.size() > 1) {
+      const LoopChain sub = slice(chain, K.begin, K.end);
+      DevChain dc = lower(sub, t);
+      std::vector<double> out(static_cast<size_t>(std::max(1, dc.nred)));
+      dev.run_untiled(dc, out.data());
+      for (size_t i = 0; i < K.red_op.size(); ++i) {
+        host_vals.at(red_base + i) = out.at(i);
+        host_known.at(red_base + i) = 1;
+      }
+      red_base += K.red_op.size();
+      rep.computed_points += sub.loops[0].range.volume();
+      rep.subchains += 1;
+      continue;
+    }
     void* fn = jit_function(K.source, K.hash, K.smem_bytes);
     const int occ = std::max(1, jit_occupancy(fn, K.nt, K.smem_bytes));
     const int64_t ns = K.segments_for(static_cast<int64_t>(dev.info().num_sms) * occ);
@@ -1151,12 +1181,16 @@ void Runtime::run_stream(const LoopChain& chain, ExecutionReport& rep, const Tar
   }
   rep.tiles_executed += rep.ctas;
   if (nred_total > 0) {
-    double *part = nullptr, *out = nullptr;
-    unsigned* ticket = nullptr;
-    dev.stream_red_buffers(1, nred_total, &part, &out, &ticket);
-    std::vector<double> r(nred_total);
-    dev.read_device(r.data(), out, nred_total);
-    for (size_t i = 0; i < nred_total; ++i) vals.at(i) = r[i];
+    bool any_dev = false;
+    for (char k : host_known) any_dev = any_dev || !k;
+    std::vector<double> r(nred_total, 0.0);
+    if (any_dev) {
+      double *part = nullptr, *out = nullptr;
+      unsigned* ticket = nullptr;
+      dev.stream_red_buffers(1, nred_total, &part, &out, &ticket);
+      dev.read_device(r.data(), out, nred_total);
+    }
+    for (size_t i = 0; i < nred_total; ++i) vals.at(i) = host_known[i] ? host_vals[i] : r[i];
   }
 }
 
@@ -1185,7 +1219,8 @@ void Runtime::check_pad(const LoopChain& chain, const Target& t) const {
 
 ExecutionReport Runtime::execute_chain(LoopChain chain, const ExecMode& mode) {
   if (distributed()) {
-    if (!chain.fills.empty()) throw InvalidArgument("periodic_fill: not supported on a rank grid");
+    if (!chain.fills.empty() && !periodic_domain_)
+      throw InvalidArgument("periodic_fill on a rank grid: call set_periodic_domain(true) before set_rank_grid");
     return execute_distributed(std::move(chain), mode);
   }
   const auto t0 = std::chrono::steady_clock::now();
@@ -1287,7 +1322,20 @@ const RankLayout& Runtime::rank_layout() {
   static thread_local RankLayout lay;
   if (fields_.empty()) throw InvalidArgument("distributed execution requires declared fields");
   Range global = fields_[0].logical;
-  for (const FieldRec& f : fields_) global = global.hull(f.logical);
+  int64_t pad = fields_[0].pad;
+  for (const FieldRec& f : fields_) {
+    global = global.hull(f.logical);
+    pad = std::min(pad, f.pad);
+  }
+  if (periodic_domain_) {
+    // the ghost layers of a periodic box are part of the decomposed domain
+    Point lo{0, 0, 0}, hi{0, 0, 0};
+    for (int d = 0; d < dim_; ++d) {
+      lo[d] = -pad;
+      hi[d] = pad;
+    }
+    global = global.dilated(lo, hi);
+  }
   lay = decompose(global, grid_);
   return lay;
 }
@@ -1518,6 +1566,83 @@ void Runtime::exchange(const DistSchedule& s, ExecutionReport& rep) {
   rep.halo_exchanges += s.msgs.empty() ? 0 : 1;
 }
 
+void Runtime::periodic_exchange(const std::vector<std::pair<DatasetId, int64_t>>& fills, ExecutionReport& rep) {
+  if (fills.empty()) return;
+  DeviceExec& dev = device();
+  const RankLayout& lay = dist_->layout;
+  const int s = dim_ - 1;
+  for (int d = 0; d < s; ++d)
+    if (lay.grid[static_cast<size_t>(d)] != 1)
+      throw InvalidArgument("periodic chains: the rank grid may split the slowest dimension only");
+  const int lo = 0, hi = lay.rank_count() - 1;  // ranks are ordered along the split dimension
+  std::vector<char> is_local(static_cast<size_t>(lay.rank_count()), 0);
+  for (int r : dist_->local) is_local[static_cast<size_t>(r)] = 1;
+  struct Move {
+    int src, dst;
+    DatasetId ds;
+    int64_t src_s0, dst_s0, n;
+  };
+  std::vector<Move> moves;
+  for (const auto& [ds, g] : fills) {
+    const FieldRec& f = fields_.at(static_cast<size_t>(ds));
+    if (g > f.pad)
+      throw AccessError("periodic chain: needs " + std::to_string(g) + " ghost layers of " + f.name + " but its pad is " +
+                        std::to_string(f.pad) + " (raise skew_allowance)");
+    const int64_t L = f.logical.start(s), H = f.logical.end(s);
+    if (lay.owned[static_cast<size_t>(hi)].start(s) > H - g || lay.owned[static_cast<size_t>(lo)].end(s) < L + g)
+      throw PlanError("periodic chain: the wrap depth exceeds an end rank's owned width");
+    // 1. faster dimensions, inside every rank, over the slabs it holds
+    for (int r : dist_->local) {
+      const Target& t = dist_->targets[static_cast<size_t>(r)];
+      const Range& a = t.alloc[static_cast<size_t>(ds)];
+      Range box = f.logical;
+      box.set_raw(s, std::max(a.start(s), L), std::min(a.end(s), H));
+      if (s > 0 && !box.empty()) dev.periodic_fill({t.dev[static_cast<size_t>(ds)]}, box, g, s);
+    }
+    // 2. the split dimension: whole slabs between the end ranks
+    moves.push_back(Move{hi, lo, ds, H - g, L - g, g});
+    moves.push_back(Move{lo, hi, ds, L, H, g});
+    // every rank's halo copies of the wrapped points are stale now
+    Point wl{0, 0, 0}, wh{0, 0, 0};
+    for (int d = 0; d < dim_; ++d) {
+      wl[d] = -g;
+      wh[d] = g;
+    }
+    dist_->written[ds].push_back(f.logical.dilated(wl, wh));
+    ++dist_->hist_version;
+  }
+  bool remote = false;
+  for (const Move& m : moves) remote = remote || (is_local[static_cast<size_t>(m.src)] != is_local[static_cast<size_t>(m.dst)]);
+  if (remote && !comm_) throw PlanError("periodic chain: remote end rank without a communicator");
+  if (remote) comm_->group_start();
+  for (const Move& m : moves) {
+    const bool ls = is_local[static_cast<size_t>(m.src)], ld = is_local[static_cast<size_t>(m.dst)];
+    if (ls && ld) continue;
+    if (ls) {
+      const int fsrc = dist_->targets[static_cast<size_t>(m.src)].dev[static_cast<size_t>(m.ds)];
+      comm_->send(dev.slab_ptr(fsrc, m.src_s0), dev.slab_count(fsrc, m.src_s0, m.src_s0 + m.n), m.dst, dev.stream());
+    } else if (ld) {
+      const int fdst = dist_->targets[static_cast<size_t>(m.dst)].dev[static_cast<size_t>(m.ds)];
+      comm_->recv(dev.slab_ptr(fdst, m.dst_s0), dev.slab_count(fdst, m.dst_s0, m.dst_s0 + m.n), m.src, dev.stream());
+      dev.note_slab_write(fdst, m.dst_s0, m.dst_s0 + m.n);
+    }
+  }
+  if (remote) comm_->group_end();
+  for (const Move& m : moves) {
+    if (!is_local[static_cast<size_t>(m.src)] || !is_local[static_cast<size_t>(m.dst)]) continue;
+    dev.copy_slabs_shift(dist_->targets[static_cast<size_t>(m.dst)].dev[static_cast<size_t>(m.ds)], m.dst_s0,
+                         dist_->targets[static_cast<size_t>(m.src)].dev[static_cast<size_t>(m.ds)], m.src_s0, m.n);
+  }
+  rep.halo_exchanges += 1;
+  rep.halo_messages += static_cast<int64_t>(moves.size());
+  for (const Move& m : moves) {
+    const FieldRec& f = fields_.at(static_cast<size_t>(m.ds));
+    int64_t plane = 1;
+    for (int d = 0; d < s; ++d) plane *= f.logical.extent(d) + 2 * m.n;
+    rep.halo_bytes += plane * m.n * 8;
+  }
+}
+
 ExecutionReport Runtime::execute_distributed(LoopChain chain, const ExecMode& mode) {
   // Tiled modes: DistContext::run_tiled (dist.cpp:617-689) -- plans + halo
   // specs for every rank, ONE deep-halo exchange, per-rank execution of the
@@ -1534,7 +1659,19 @@ ExecutionReport Runtime::execute_distributed(LoopChain chain, const ExecMode& mo
   ensure_dist();
   DeviceExec& dev = device();
   const int64_t l0 = dev.launches();
-  const bool on_demand = mode.kind == ExecMode::Kind::Untiled;
+  bool on_demand = mode.kind == ExecMode::Kind::Untiled;
+  if (!chain.fills.empty()) {
+    // Periodic marks on a rank grid: wrap the chain's inputs once (faster
+    // dimensions inside every rank, the split dimension between the end
+    // ranks), then the deep-halo schedule of the rewritten chain -- whatever
+    // the mode (the on-demand per-loop exchange does not own the ghost zones).
+    std::vector<Range> logical;
+    for (const FieldRec& f : fields_) logical.push_back(f.logical);
+    PeriodicPlan pp = apply_periodic(chain, logical);
+    periodic_exchange(pp.pre_fills, rep);
+    chain = std::move(pp.chain);
+    on_demand = false;
+  }
   if (poison_) poison_stale_halos(chain);
   // Stages: (schedule, loops [begin, end) of the chain it covers).
   std::vector<std::shared_ptr<const DistSchedule>> stages;
@@ -1808,7 +1945,8 @@ Range Runtime::local_box(DatasetId ds) {
 }
 
 void Runtime::periodic_fill(const std::vector<DatasetId>& list, int64_t depth) {
-  if (distributed()) throw InvalidArgument("periodic_fill: not supported on a rank grid");
+  if (distributed() && (periodic_flush_ || !periodic_domain_))
+    throw InvalidArgument("periodic_fill on a rank grid: needs set_periodic_domain(true) and recorded (not eager) fills");
   if (depth < 0) throw InvalidArgument("periodic_fill: negative depth");
   if (recording_) {
     RecordedCall rc;

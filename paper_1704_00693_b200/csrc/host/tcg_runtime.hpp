@@ -114,6 +114,14 @@ class Runtime {
   // false (default): it records a PeriodicMark in the queue and the chain is
   // rewritten at flush (tcg_periodic.hpp) -- one wrap per chain.
   void set_periodic_flush(bool v) { periodic_flush_ = v; }
+  // Periodic box on a rank grid (call before set_rank_grid / set_process_rank):
+  // the decomposed domain is the fields' logical hull dilated by the smallest
+  // field pad, so the ghost layers belong to the end ranks, the rewritten
+  // chain's extended loops stay inside the domain, and the wrap along the
+  // split (slowest) dimension is a slab message between the end ranks -- the
+  // "self-exchange" at one rank. The grid may split the slowest dimension only.
+  void set_periodic_domain(bool v);
+  bool periodic_domain() const { return periodic_domain_; }
   // Order-matched Sum reductions: chains with a Sum reduction run on the
   // untiled executor and fold in the reference's order for a pool of
   // `workers` threads (executor.cpp:55-61 static spans, :141-144 sequential
@@ -221,6 +229,7 @@ class Runtime {
   void drop_dist();
   std::shared_ptr<const DistSchedule> dist_schedule(const LoopChain& chain);
   void exchange(const DistSchedule& s, ExecutionReport& rep);
+  void periodic_exchange(const std::vector<std::pair<DatasetId, int64_t>>& fills, ExecutionReport& rep);
   void poison_stale_halos(const LoopChain& chain);
   bool poison_ = false;  // TCG_POISON_HALOS=1 (debug tripwire, dist.cpp:546-586)
   int root_for(DatasetId ds, const Point& p);
@@ -262,6 +271,7 @@ class Runtime {
   std::vector<RecordedCall> record_cur_;
   std::vector<std::vector<RecordedCall>> recorded_;
   bool periodic_flush_ = false;
+  bool periodic_domain_ = false;
   int red_workers_ = 0;
   std::unordered_set<uint64_t> body_sig_ok_;  // (body, declaration) pairs the probe accepted
   ExecMode default_mode_;

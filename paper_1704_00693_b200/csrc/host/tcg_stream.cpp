@@ -900,6 +900,15 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
   for (size_t v = 0; v < Sc.vers.size(); ++v)
     if (Sc.vers[v].needed && Sc.vers[v].prod < 0)
       (Sc.vers[v].tma ? tma : (Sc.vers[v].cpa ? cpa : loaded)).push_back(static_cast<int>(v));
+  // Neighbour synchronisation (TCG_STREAM_NSYNC): a warp reads only the
+  // shared-memory rows of the warps within the chain's in-plane reach, so the
+  // per-step CTA barrier becomes one mbarrier per warp -- each warp arrives at
+  // the end of its step (its writes published, its reads done) and waits, at
+  // the top of the next step, for the warps it reads from. Warps then run up
+  // to a step apart instead of in lock step.
+  const int nwarps = S.nt / 32;
+  const bool nsync = env_int(A.dim == 2 ? "TCG_STREAM_NSYNC2" : "TCG_STREAM_NSYNC3", env_int("TCG_STREAM_NSYNC", 0)) != 0 &&
+                     tma.empty() && nwarps > 1 && S.nt % 32 == 0 && !(S.blk.strided && BX > 1);
   const int rows_per = A.dim == 3 ? S.ty : 1;
   const int nrows = static_cast<int>(tma.size()) * rows_per;  // bulk copies per step
   const int nissue = std::min(nrows, S.nt);                     // threads issuing them
@@ -1278,8 +1287,17 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
       steps << "    if (t - " << Sc.la << " >= tstart) tcgj::mbar_wait(&bar[" << (((u - Sc.la) % Sc.nbar + Sc.nbar) % Sc.nbar)
             << "], static_cast<unsigned>(((t - " << Sc.la << " - tstart) / " << Sc.nbar << ") & 1));\n";
     }
-    if (!cpa.empty()) steps << "    tcgj::cp_async_wait<" << (Sc.la - 1) << ">();\n";
-    steps << "    __syncthreads();\n";
+    if (nsync) {
+      // Two barriers per warp, alternating by step: a neighbour can complete
+      // at most one more phase of the SAME barrier only after it has seen
+      // this warp's next arrival, so the parity test cannot alias.
+      steps << "    if (t > tstart) {\n      const int k_ = t - 1 - tstart;\n"
+            << "      const unsigned par_ = static_cast<unsigned>((k_ >> 1) & 1);\n"
+            << "      for (int w_ = nlo_; w_ <= nhi_; ++w_)\n        if (w_ != warp_) tcgj::mbar_wait(&nbar[2 * w_ + (k_ & 1)], par_);\n    }\n";
+    } else {
+      if (!cpa.empty()) steps << "    tcgj::cp_async_wait<" << (Sc.la - 1) << ">();\n";
+      steps << "    __syncthreads();\n";
+    }
     // asynchronous inputs: the row that becomes readable this step enters the register ring
     for (size_t v = 0; v < Sc.vers.size(); ++v) {
       const SVer& sv = Sc.vers[v];
@@ -1297,6 +1315,10 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
       }
     }
     emit_step(steps, u);
+    if (nsync) {
+      if (!cpa.empty()) steps << "    tcgj::cp_async_wait<" << (Sc.la - 1) << ">();\n";
+      steps << "    __syncwarp();\n    if ((tid & 31) == 0) tcgj::mbar_arrive(&nbar[2 * warp_ + ((t - tstart) & 1)]);\n";
+    }
     steps << "    }\n    }\n";
   }
   o << "  const unsigned m_own = tcgj::cmask<P, BX, SX>(cx0, cy0, ox0, ox1, oy0, oy1);\n  (void)m_own;\n";
@@ -1313,6 +1335,20 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
   }
   for (size_t r = 0; r < accs.size(); ++r) o << "  double " << accs[r] << " = tcgj::ident(" << red_ops[r] << ");\n";
   o << ptrs.str();
+  if (nsync) {
+    o << "  __shared__ __align__(8) unsigned long long nbar[" << 2 * nwarps << "];\n";
+    o << "  const int warp_ = tid >> 5;\n";
+    if (S.blk.strided) {
+      o << "  const int nlo_ = max(0, (32 * warp_ - " << S.rx << ") / 32), nhi_ = min(" << (nwarps - 1) << ", (32 * warp_ + 31 + "
+        << S.rx << ") / 32);\n";
+    } else {
+      const int dyr = A.dim == 3 ? (S.ry + S.blk.by - 1) / S.blk.by : 0;
+      o << "  const int nlo_ = max(0, ((32 * warp_) / NTX - " << dyr << ") * NTX / 32), nhi_ = min(" << (nwarps - 1)
+        << ", (((32 * warp_ + 31) / NTX + " << dyr << ") * NTX + NTX - 1) / 32);\n";
+    }
+    o << "  if (tid == 0) {\n    for (int i = 0; i < " << 2 * nwarps << "; ++i) tcgj::mbar_init(&nbar[i], 1);\n";
+    o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n  __syncthreads();\n";
+  }
   if (Sc.nbar) {
     o << "  if (tid == 0) {\n    for (int i = 0; i < " << Sc.nbar << "; ++i) tcgj::mbar_init(&bar[i], " << nissue << ");\n";
     o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n  __syncthreads();\n";
@@ -1408,6 +1444,39 @@ int64_t StreamKernel::segments_for(int64_t slots) const {
   int64_t ns = tiles >= slots ? (dim == 3 ? 4 : 1) : slots / tiles;
   ns = std::min<int64_t>(ns, std::max<int64_t>(1, stream_extent / min_seg));
   return std::max<int64_t>(1, ns);
+}
+
+std::string StreamKernel::cta_text(int64_t ns) const {
+  std::ostringstream o;
+  if (nctas == 0 && tiles <= 1 && hull.dim() == 0) return o.str();
+  const int s = dim - 1;
+  const int64_t nxt = grid[0], nyt = dim == 3 ? grid[1] : 1;
+  int64_t idx = 0;
+  for (int64_t iseg = 0; iseg < ns; ++iseg)
+    for (int64_t ity = 0; ity < nyt; ++ity)
+      for (int64_t itx = 0; itx < nxt; ++itx, ++idx) {
+        Range own(dim);
+        const int64_t ox0 = hull.start(0) + itx * owned[0];
+        own.set_raw(0, ox0, std::min(ox0 + owned[0], hull.end(0)));
+        if (dim == 3) {
+          const int64_t oy0 = hull.start(1) + ity * owned[1];
+          own.set_raw(1, oy0, std::min(oy0 + owned[1], hull.end(1)));
+        }
+        const int64_t ext = hull.extent(s);
+        own.set_raw(s, hull.start(s) + iseg * ext / ns, hull.start(s) + (iseg + 1) * ext / ns);
+        for (size_t l = 0; l < loop_range.size(); ++l) {
+          Range r(dim);
+          for (int d = 0; d < dim; ++d) r.set_raw(d, 0, 0);
+          if (loop_live[l] && !own.empty()) {
+            r = own;
+            for (int d = 0; d < dim; ++d)
+              r.set_raw(d, own.start(d) - loop_need[l][static_cast<size_t>(2 * d)], own.end(d) + loop_need[l][static_cast<size_t>(2 * d + 1)]);
+            r = r.intersect(loop_range[l]);
+          }
+          o << "cta=" << idx << " loop=" << (begin + l) << " owned=" << own.to_string() << " range=" << r.to_string() << "\n";
+        }
+      }
+  return o.str();
 }
 
 std::string StreamPlan::summary() const {
@@ -1555,6 +1624,15 @@ StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeo
     for (size_t li = 0; li < sub.size(); ++li) {
       K.recorded_points += sub.loops[li].range.volume();
       nloops_live += A.loops[li].needed ? 1 : 0;
+    }
+    K.hull = A.H;
+    for (size_t li = 0; li < sub.size(); ++li) {
+      K.loop_range.push_back(sub.loops[li].range);
+      K.loop_live.push_back(A.loops[li].needed ? 1 : 0);
+      std::array<int64_t, 6> nd6{0, 0, 0, 0, 0, 0};
+      for (int d = 0; d < A.dim; ++d)
+        for (int e = 0; e < 2; ++e) nd6[static_cast<size_t>(2 * d + e)] = std::max<int64_t>(0, A.loops[li].need[d][e]);
+      K.loop_need.push_back(nd6);
     }
     K.tiles = S.nxt * S.nyt;
     K.stream_extent = A.H.extent(A.s);

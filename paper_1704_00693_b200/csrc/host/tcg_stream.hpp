@@ -25,6 +25,7 @@
 // Datasets a chain both reads and rewrites are written to their second
 // buffer (ping-pong) so no CTA can observe another CTA's writes.
 #pragma once
+#include <array>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -96,6 +97,15 @@ struct StreamKernel {
   int64_t tile_points = 1;        // computed cross-section points per CTA
   int live_loops = 0;
   int forced_segments = 0;        // StreamChoice::segments
+  // Schedule export (validators): the owned hull, the per-loop ranges and the
+  // extension each live loop is computed over beyond a CTA's owned box.
+  Range hull;
+  std::vector<Range> loop_range;
+  std::vector<uint8_t> loop_live;
+  std::vector<std::array<int64_t, 6>> loop_need;  // [d * 2 + side]
+  // CTA plans as text, one line per (CTA, loop): "cta=<i> loop=<l> owned=<box> range=<box>"
+  // (range empty for loops the kernel does not execute), for ns stream segments.
+  std::string cta_text(int64_t ns) const;
   int64_t segments_for(int64_t slots) const;
   int64_t computed_for(int64_t ns) const { return live_loops * tiles * tile_points * (stream_extent + ns * warm_rows); }
 };

@@ -244,6 +244,7 @@ int tcg_stream_plan_pending(tcg_runtime* rt, int what, char* buf, int64_t n, int
         if (!log.empty()) out += log + "\n";
       }
       if (what & 2) out += "----- source kernel " + std::to_string(i) + "\n" + k.source;
+      if ((what & 4) && k.nctas) out += "----- ctas kernel " + std::to_string(i) + "\n" + k.cta_text(k.grid[2]);
     }
     put_text(out, buf, n, needed);
   });
@@ -389,6 +390,10 @@ int tcg_replay(tcg_runtime* rt, int32_t id, const double* params, int64_t nparam
     if (nhandles) *nhandles = static_cast<int64_t>(hs.size());
     for (size_t i = 0; i < hs.size() && static_cast<int64_t>(i) < max_handles; ++i) handles[i] = hs[i].id;
   });
+}
+
+int tcg_set_periodic_domain(tcg_runtime* rt, int on) {
+  return guard([&] { rt->rt->set_periodic_domain(on != 0); });
 }
 
 int tcg_set_periodic_flush(tcg_runtime* rt, int flush_each) {

@@ -108,6 +108,7 @@ def load_library() -> ctypes.CDLL:
         "tcg_set_rank_grid": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
         "tcg_periodic_fill": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_I32), _I64]),
         "tcg_set_periodic_flush": (ctypes.c_int, [_P, ctypes.c_int]),
+        "tcg_set_periodic_domain": (ctypes.c_int, [_P, ctypes.c_int]),
         "tcg_set_reduction_order": (ctypes.c_int, [_P, ctypes.c_int]),
         "tcg_record_begin": (ctypes.c_int, [_P]),
         "tcg_record_end": (ctypes.c_int, [_P, ctypes.POINTER(_I32)]),
@@ -561,6 +562,11 @@ class Runtime:
             _check(self._lib.tcg_replay(self._h, template, arr, len(params), hs, 16, ctypes.byref(n)))
         return [hs[i] for i in range(min(n.value, 16))]
 
+    def set_periodic_domain(self, on: bool = True) -> None:
+        """Periodic box on a rank grid: call before set_rank_grid /
+        set_process_rank (the ghost layers join the decomposed domain)."""
+        _check(self._lib.tcg_set_periodic_domain(self._h, 1 if on else 0))
+
     def set_periodic_flush(self, flush_each: bool) -> None:
         _check(self._lib.tcg_set_periodic_flush(self._h, 1 if flush_each else 0))
 
@@ -616,11 +622,11 @@ class Runtime:
         _check(self._lib.tcg_set_stream_choice(self._h, _arr(_I32, [nt, bx, by, ntx, segments, max_loops, minb,
                                                                     prefetch])))
 
-    def stream_plan_pending(self, compile: bool = False, source: bool = False, size: int = 1 << 26) -> str:
+    def stream_plan_pending(self, compile: bool = False, source: bool = False, size: int = 1 << 26, ctas: bool = False) -> str:
         """Streaming plan of the pending chain (consumed): summary lines, plus
         the NVRTC compile log (compile=True; no GPU needed) and the generated
         sources (source=True)."""
-        return _text(self._lib.tcg_stream_plan_pending, self._h, (1 if compile else 0) | (2 if source else 0),
+        return _text(self._lib.tcg_stream_plan_pending, self._h, (1 if compile else 0) | (2 if source else 0) | (4 if ctas else 0),
                      size=size)
 
     def gpu_plan_pending(self, mode: ExecMode, size: int = 1 << 26) -> str:

@@ -40,6 +40,9 @@ SIZES = {
     # Sum mode (Runtime.set_reduction_order(threads)), which reproduces the
     # reference's worker fold, so all 200 iterations must agree.
     "c4_ordered": {"n": 4096, "iters": 200, "threads": 8},
+    # c5 (BASELINE 768^3 needs 62 GB of host fields): the largest size this
+    # container's reference run holds comfortably; logical boxes hashed.
+    "c5": {"n": 256, "steps": 2},
 }
 
 
@@ -66,6 +69,10 @@ def run(name: str, rt, size: dict):
             c.enqueue_chain()
             rt.flush()
         return c.outputs(), []
+    if name == "c5":
+        c = configs.NsC5(rt, size["n"])
+        kes = [rt.fetch_reduction(c.enqueue_step()) for _ in range(size["steps"])]
+        return c.outputs(), kes
     if name in ("c4", "c4_ordered"):
         c = configs.CgC4(rt, size["n"])
         c.start()
@@ -84,7 +91,7 @@ def main(argv):
         size = SIZES[name]
         t0 = time.time()
         threads = size.get("threads", os.cpu_count() or 1)
-        rt = po.RefRuntime(3 if name == "c3" else 2, threads=threads)
+        rt = po.RefRuntime(3 if name in ("c3", "c5") else 2, threads=threads)
         rt.set_default_mode(ExecMode.untiled())
         fields, hist = run(name, rt, size)
         out[name] = {

@@ -220,10 +220,12 @@ dist.destroy_process_group()
 def test_two_process_nccl_z_split(tmp_path, mode):
     # One rank per process / GPU, the deep-halo exchange carried by
     # ncclSend/ncclRecv straight from the field slabs. Needs two GPUs.
-    import torch
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
     import subprocess, sys, os
+    # (torch must not be imported here: libtcg is linked against the system
+    # NCCL and is already loaded; the children import torch first.)
+    ngpu = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True).stdout.count("GPU ")
+    if ngpu < 2:
+        pytest.skip("needs 2 GPUs")
     from pathlib import Path
     repo = str(Path(__file__).resolve().parent.parent)
     script = tmp_path / "two_rank.py"

@@ -36,7 +36,7 @@ MODES = {
 
 
 def _run(name, mode):
-    rt = Runtime(3 if name == "c3" else 2)
+    rt = Runtime(3 if name in ("c3", "c5") else 2)
     rt.set_default_mode(mode)
     fields, hist = G.run(name, rt, GOLD[name]["size"])
     shas = {k: G.field_sha(v) for k, v in fields.items()}
@@ -99,3 +99,17 @@ def test_order_matched_sum_small_matches_reference_threads(ref_lib):
             cr.iterate()
             cg.iterate()
         assert [float(x).hex() for x in cg.history] == [float(x).hex() for x in cr.history], threads
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_c5_at_256_cubed_matches_reference(mode):
+    # c5 against the unmodified reference at 256^3 (periodic ghosts by host
+    # copy there, recorded marks + one wrap per chain here): conserved fields
+    # bit-exact over the logical box, kinetic energy (a Sum) to 1e-12.
+    shas, kes = _run("c5", MODES[mode]())
+    want = GOLD["c5"]
+    assert shas == want["fields"]
+    ref = [float.fromhex(x) for x in want["history"]]
+    assert len(kes) == len(ref)
+    for a, b in zip(kes, ref):
+        assert abs(a - b) <= 1e-12 * abs(b)

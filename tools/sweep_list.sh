@@ -1,20 +1,16 @@
 # cfg: nt,bx,by,ntx,segments,max_loops,minb,prefetch
-run c2 ob0 "" TCG_STREAM_OWN_BUDGET=0
-run c2 ob8 "" TCG_STREAM_OWN_BUDGET=8
-run c2 ob16 "" TCG_STREAM_OWN_BUDGET=16
-run c2 ob24 "" TCG_STREAM_OWN_BUDGET=24
-run c2 ob20 "" TCG_STREAM_OWN_BUDGET=20
-run c2 ob16la2 "" TCG_STREAM_OWN_BUDGET=16 TCG_STREAM_LOOKAHEAD=2
-run c2 ob24la2 "" TCG_STREAM_OWN_BUDGET=24 TCG_STREAM_LOOKAHEAD=2
-run c1 ob0 "" TCG_STREAM_OWN_BUDGET=0
-run c1 ob8 "" TCG_STREAM_OWN_BUDGET=8
-run c1 ob16 "" TCG_STREAM_OWN_BUDGET=16
-run c4 ob0 "" TCG_STREAM_OWN_BUDGET=0
-run c4 ob16 "" TCG_STREAM_OWN_BUDGET=16
-run c3 lcm12 "0,0,0,0,3,3,0,0" TCG_STREAM_LCM_UNROLL=12
-run c3 lcm12la2 "0,0,0,0,3,3,0,0" TCG_STREAM_LCM_UNROLL=12 TCG_STREAM_LOOKAHEAD=2
-run c3 s4 "0,0,0,0,4,3,0,0"
-run c3 by4s3 "256,1,4,32,3,3,0,0"
-run c3 by4s3lcm "256,1,4,32,3,3,0,0" TCG_STREAM_LCM_UNROLL=12
-run c3 h2s3 "0,0,0,0,3,2,0,0"
-run c3 h4s3 "0,0,0,0,3,4,0,0" TCG_STREAM_RMAX3=3
+run c3 base ""
+run c3 ns1 "" TCG_STREAM_NSYNC=1
+run c3 ns1la2 "" TCG_STREAM_NSYNC=1 TCG_STREAM_LOOKAHEAD=2
+run c3 ns1la4 "" TCG_STREAM_NSYNC=1 TCG_STREAM_LOOKAHEAD=4
+run c3 ns1by4 "256,1,4,32,0,3,0,0" TCG_STREAM_NSYNC=1
+run c3 ns1h4 "0,0,0,0,0,4,0,0" TCG_STREAM_NSYNC=1 TCG_STREAM_RMAX3=3
+run c3 ns1f1 "" TCG_STREAM_NSYNC=1 TCG_STREAM_FAST=1
+run c2 base ""
+run c2 ns1 "" TCG_STREAM_NSYNC=1
+run c2 ns1n256 "256,0,0,0,0,0,0,0" TCG_STREAM_NSYNC=1
+run c2 ns1n192 "192,0,0,0,0,0,0,0" TCG_STREAM_NSYNC=1
+run c1 base ""
+run c1 ns1 "" TCG_STREAM_NSYNC=1
+run c5 base ""
+run c5 ns1 "" TCG_STREAM_NSYNC=1
