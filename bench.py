@@ -231,7 +231,7 @@ WORKLOAD_TEXT = {
 }
 
 
-SHARDED = {"c2": 1, "c3": 2}  # config -> dimension its domain is split along at N > 1
+SHARDED = {"c2": 1, "c3": 2, "c5": 2}  # config -> dimension its domain is split along at N > 1
 
 
 def workload_text(name, world):
@@ -406,10 +406,10 @@ def main():
     torch.cuda.set_device(local)
     mode = parse_mode(args.mode)
 
-    # N > 1: c2 (along y) and c3 (along z) split the BASELINE domain across the
-    # GPUs -- strong scaling, one rank per process, one deep-halo exchange per
-    # chain over NCCL; c1 / c4 / c5 run as independent replicas (c5's periodic
-    # wrap is not available on a rank grid yet).
+    # N > 1: c2 (along y), c3 and c5 (along z) split the BASELINE domain across
+    # the GPUs -- strong scaling, one rank per process, one deep-halo exchange
+    # per chain over NCCL (c5: plus one periodic wrap between the end ranks,
+    # DESIGN.md §6); c1 / c4 run as independent replicas.
     sharded = (world > 1 or args.shard) and args.config in SHARDED
 
     def new_comm_id():
@@ -422,6 +422,8 @@ def main():
     def build(m):
         rt = Runtime(3 if args.config in ("c3", "c5") else 2)
         if sharded:
+            if args.config == "c5":
+                rt.set_periodic_domain(True)  # ghost layers owned by the end ranks
             grid = [1, 1, 1]
             grid[SHARDED[args.config]] = world
             rt.set_process_rank(tuple(grid), rank, new_comm_id())
@@ -478,8 +480,12 @@ def main():
                           f"({ms_instr / args.steps:.4f} ms/step instrumented)",
                 "compulsory_bytes_per_launch": comp * args.steps / max(kn, 1),
                 "frac_compulsory": (comp * args.steps / max(kn, 1)) / (avg_ms / 1e3) / 1e9 / peak if kn else None,
-                "note": "achieved = untiled-chain (algorithmic) bytes / kernel time; >1 means on-chip reuse. "
-                        "frac_compulsory uses the bytes a fully fused chain must move."}
+                "dram_GBps_from_traffic": (traffic / (avg_ms / 1e3) / 1e9) if (traffic and kn) else None,
+                "frac_traffic": (traffic / (avg_ms / 1e3) / 1e9 / peak) if (traffic and kn) else None,
+                "note": "achieved = untiled-chain (algorithmic) bytes / kernel time (SURVEY.md 8(d) effective GB/s); "
+                        "a fused kernel keeps intermediates on chip, so frac > 1 is the fusion gain, not an HBM rate. "
+                        "The HBM-side fractions of the same kernel: frac_compulsory (bytes a fully fused chain must "
+                        "move / time / peak) and frac_traffic (committed ncu DRAM bytes per launch / time / peak)."}
 
     # ---- untiled executor on the same inputs (tiled-vs-untiled speedup) -------
     del rt, cfg, step

@@ -1415,6 +1415,13 @@ std::shared_ptr<const DistSchedule> Runtime::dist_schedule(const LoopChain& chai
 DistSchedule Runtime::schedule_pending() {
   if (!grid_set_) throw InvalidArgument("schedule_pending: no rank grid set");
   LoopChain chain = take_pending();
+  if (!chain.fills.empty()) {
+    if (!periodic_domain_)
+      throw InvalidArgument("periodic_fill on a rank grid: call set_periodic_domain(true) before set_rank_grid");
+    std::vector<Range> logical;
+    for (const FieldRec& f : fields_) logical.push_back(f.logical);
+    chain = apply_periodic(chain, logical).chain;
+  }
   if (!dist_) {
     // Host-only use (no device): layout and history without rank fields.
     auto d = std::make_unique<Dist>();

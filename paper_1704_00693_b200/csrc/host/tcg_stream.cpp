@@ -1088,9 +1088,10 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
     // step is one straight-line block -- no per-loop range branches or
     // pass-through selects -- so the compiler overlaps the shared-memory
     // reads and the fp64 chains of all loops.
-    // Measured on B200 (profiles/r5): slower in 2D (c2 0.56 -> 0.70 ms/step: the long step body doubles),
-    // neutral in 3D; off by default.
-    const bool step_fast = env_int(A.dim == 2 ? "TCG_STREAM_FAST2" : "TCG_STREAM_FAST3", env_int("TCG_STREAM_FAST", 0)) != 0;
+    // Measured on B200 (profiles/r5/sweeps.md): slower in 2D (c2 0.56 -> 0.70 ms/step: the long step
+    // body doubles in size), 3-8% faster in 3D (c3 7.14 -> 6.56 ms/chain): on in 3D only.
+    const bool step_fast =
+        env_int(A.dim == 2 ? "TCG_STREAM_FAST2" : "TCG_STREAM_FAST3", env_int("TCG_STREAM_FAST", A.dim == 3 ? 1 : 0)) != 0;
     auto emit_loops = [&](bool all_fast) {
     size_t racc = 0;
     for (size_t li = 0; li < ch.loops.size(); ++li) {

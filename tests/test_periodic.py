@@ -85,3 +85,30 @@ def test_mark_extends_the_producer_and_wraps_its_input():
     text = rt.periodic_plan_pending()
     assert _ranges(text) == [(-1, 17), (0, 16)]
     assert re.findall(r"wrap ds=(\d+) depth=(\d+)", text) == [(str(b), "1")]
+
+
+def test_c5_rank_grid_schedule_covers_the_extended_loops(monkeypatch):
+    # Periodic box on a rank grid (host-only): the ghost layers join the
+    # decomposed domain, so the union of the ranks' loop ranges is each
+    # extended loop range of the rewritten chain (the end ranks compute the
+    # ghost zones) and interior faces keep the usual deep-halo messages.
+    from paper_1704_00693_b200 import RuntimeConfig
+    monkeypatch.setattr(configs.NsC5, "_initial", lambda self, sb: {})
+    rt = _host_only(Runtime(3, RuntimeConfig(skew_allowance=6)))
+    rt.set_periodic_domain(True)
+    rt.set_rank_grid((1, 1, 4))
+    c = configs.NsC5(rt, 48)
+    c.enqueue_step()
+    sched = rt.schedule_pending()
+    ext = [6] + [4] * 6 + [4] + [2] * 6 + [2] + [0] * 7
+    assert len(sched["ranks"]) == 4
+    # pad = 2 + 6 = 8: domain [-8, 56)^3, 16 planes per rank
+    assert sched["ranks"][0]["owned"] == "[-8,56)x[-8,56)x[-8,8)"
+    for l, e in enumerate(ext):
+        zlo = min(r["loops"][l][2][0] for r in sched["ranks"].values() if r["loops"][l][2][1] > r["loops"][l][2][0])
+        zhi = max(r["loops"][l][2][1] for r in sched["ranks"].values() if r["loops"][l][2][1] > r["loops"][l][2][0])
+        assert (zlo, zhi) == (-e, 48 + e), (l, zlo, zhi)
+        for r in sched["ranks"].values():
+            (x0, x1), (y0, y1), _ = r["loops"][l]
+            assert (x0, x1, y0, y1) == (-e, 48 + e, -e, 48 + e)
+    assert all(m["dim"] == 2 for m in sched["msgs"]) and len(sched["msgs"]) > 0
