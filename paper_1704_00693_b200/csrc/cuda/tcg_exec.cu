@@ -48,11 +48,8 @@ struct ULaunch {
   // stencils' offsets per dimension, and the mask of arguments that read.
   int32_t pf, rmask;
   int32_t rlo[3], rhi[3];
-  // Staged 3D walk (k_untiled3s): tile rows (TY) and planes per block (ZR),
-  // shared-memory ring base (doubles) of each reading argument.
-  int32_t sty, szr, sslots;
+  int32_t pad3_[3];
   int32_t band;  // 3D: y-blocks per rasterisation band (block_yz), 0 = hardware order
-  int32_t sring[kMaxArgs];
 #ifdef TCG_CHECKED
   int64_t alo[kMaxArgs][3], ahi[kMaxArgs][3];  // allocation of each argument
 #endif
@@ -418,238 +415,6 @@ template <int BODY, int kUntiledRun = 4>
 __global__ void __launch_bounds__(256, 6) k_untiled2(const __grid_constant__ ULaunch L) {
   untiled_block<2, BODY, kUntiledRun>(L);
 }
-
-// ---------------------------------------------------------------------------
-// Staged 3D untiled walk (2.5D): a block owns a kS3X x TY column of points
-// and walks ZR planes of it. Every reading argument keeps a ring of kS3Slots
-// planes of its (kS3X + 6) x (TY + 4) tile (halo 2 + alignment) in shared
-// memory, filled by cp.async.bulk row copies (TMA bulk engine, mbarrier
-// completion): while plane z is computed from shared memory, plane
-// z + 1 + rhi_z is in flight. Stencil reads are shared-memory loads at
-// compile-time offsets; writes go straight to HBM. Loops with stencil reach
-// <= 2 per dimension (c3's 7-point star, c5's radius-2 stars).
-namespace s3 {
-constexpr int kS3X = 32;      // tile width (one warp per row)
-constexpr int kS3W = kS3X + 6;  // smem row pitch: halo 2 each side + 2 alignment slack
-constexpr int kS3MaxSlots = 12;  // ring planes: up to 5 in use + planes in flight
-
-__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void mb_init(uint64_t* m, unsigned c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(m)), "r"(c) : "memory");
-}
-__device__ __forceinline__ void mb_expect(uint64_t* m, unsigned b) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(su32(m)), "r"(b) : "memory");
-}
-__device__ __forceinline__ void mb_arrive(uint64_t* m) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(su32(m)) : "memory");
-}
-// Waits for the phase of parity `par`; traps (a launch error, not a hung
-// GPU) if the copies never land.
-__device__ __forceinline__ void mb_wait(uint64_t* m, unsigned par) {
-  const long long t0 = clock64();
-  for (;;) {
-    uint32_t done;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(su32(m)), "r"(par)
-        : "memory");
-    if (done) return;
-    if (clock64() - t0 > (1ll << 32)) __trap();  // ~2 s at 1.9 GHz
-  }
-}
-__device__ __forceinline__ void g2s(void* dst, const void* src, unsigned bytes, uint64_t* m) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(m))
-               : "memory");
-}
-
-// Accessor: reads from the plane rings, writes / increments to HBM.
-struct SAcc {
-  const ULaunch& L;
-  const double* sm;
-  int ctr;        // (ly, lx) offset of the point inside a plane tile
-  int pofs[5];    // ring offset (doubles) of plane z + dz, dz = -2..2
-  double* g[kMaxArgs];
-  int64_t px, py, pz;
-  double acc;
-  __device__ __forceinline__ int64_t x() const { return px; }
-  __device__ __forceinline__ int64_t y() const { return py; }
-  __device__ __forceinline__ int64_t z() const { return pz; }
-  __device__ __forceinline__ double read(int a, int dx, int dy, int dz) const {
-    return sm[L.sring[a] + pofs[dz + 2] + ctr + dy * kS3W + dx];
-  }
-  __device__ __forceinline__ void write(int a, double v) const { *g[a] = v; }
-  __device__ __forceinline__ void increment(int a, double v) const { *g[a] = read(a, 0, 0, 0) + v; }
-  __device__ __forceinline__ void contribute(double v) {
-    if (L.masked && (px < L.mlo[0] || px >= L.mhi[0] || py < L.mlo[1] || py >= L.mhi[1] || pz < L.mlo[2] ||
-                     pz >= L.mhi[2]))
-      return;
-    acc = red_combine(L.red_op, acc, v);
-  }
-  __device__ __forceinline__ int nargs() const { return L.nargs; }
-  __device__ __forceinline__ int mode(int a) const { return L.a[a].mode; }
-  __device__ __forceinline__ int npts(int a) const { return L.st.npts[L.a[a].stencil]; }
-  __device__ __forceinline__ int pt(int a, int j, int d) const {
-    return L.st.pts[3 * (L.st.start[L.a[a].stencil] + j) + d];
-  }
-  __device__ __forceinline__ bool reduces() const { return L.has_red != 0; }
-};
-}  // namespace s3
-
-template <int BODY>
-__global__ void __launch_bounds__(256) k_untiled3s(const __grid_constant__ ULaunch L) {
-  using namespace s3;
-  extern __shared__ __align__(16) double sm[];
-  __shared__ uint64_t mbar[kS3MaxSlots];
-  const int TY = L.sty, S = L.sslots;
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = tx + kS3X * ty, nth = kS3X * TY;
-  const int64_t xe = L.lo[0] + L.n[0], ye = L.lo[1] + L.n[1], ze = L.lo[2] + L.n[2];
-  const int64_t xb = L.lo[0] + static_cast<int64_t>(blockIdx.x) * kS3X;
-  const int64_t yb = L.lo[1] + static_cast<int64_t>(blockIdx.y) * TY;
-  const int64_t zb = L.lo[2] + static_cast<int64_t>(blockIdx.z) * L.szr;
-  const int64_t zend = min(zb + L.szr, ze);
-  const int plane = (TY + 4) * kS3W;  // doubles per ring plane
-  // Column origin of the tiles: x = xb - 2 - s at column 0, s making the
-  // first copied element 16-byte aligned (field rows start 128-B aligned at
-  // x0, a multiple of 16 elements; every field shares that parity).
-  const UArg& a0 = L.a[__ffs(static_cast<unsigned>(L.rmask)) - 1];
-  const int sh = static_cast<int>((xb - 2 - a0.x0) & 1);
-  const int64_t gx0 = xb - 2 - sh;
-  // Copied box per plane (the loop's read hull over the block).
-  const int64_t cx0 = xb + L.rlo[0], cx1 = min(xb + kS3X, xe) + L.rhi[0];
-  const int c0 = static_cast<int>((cx0 - gx0) & ~int64_t{1});
-  const int c1 = static_cast<int>((cx1 - gx0 + 1) & ~int64_t{1});
-  const unsigned rbytes = static_cast<unsigned>(c1 - c0) * 8u;
-  const int64_t ry0 = yb + L.rlo[1], ry1 = min(yb + TY, ye) + L.rhi[1];
-  const int nrows = static_cast<int>(ry1 - ry0);
-  const int nread = __popc(static_cast<unsigned>(L.rmask));
-  const int64_t pbase = zb + L.rlo[2];           // first plane read; ring slot of plane p: (p - pbase) mod S
-  const int64_t plast = zend - 1 + L.rhi[2];     // last plane the block reads
-  const int D = S - (L.rhi[2] - L.rlo[2] + 1);   // planes loaded ahead of use
-  if (tid == 0) {
-    for (int i = 0; i < S; ++i) mb_init(&mbar[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto slot_of = [&](int64_t p) { return static_cast<int>((p - pbase) % S); };
-  auto parity_of = [&](int64_t p) { return static_cast<unsigned>(((p - pbase) / S) & 1); };
-  // Copies of plane p into its ring slot (row copies spread over threads).
-  auto load_plane = [&](int64_t p) {
-    const int slot = slot_of(p);
-    for (int i = tid; i < nread * nrows; i += nth) {
-      const int k = i / nrows, r = i - k * nrows;
-      unsigned m = static_cast<unsigned>(L.rmask);
-      for (int j = 0; j < k; ++j) m &= m - 1;
-      const int a = __ffs(m) - 1;
-      const UArg& g = L.a[a];
-      const int64_t yy = ry0 + r;
-      const double* src = g.base + ((p - g.z0) * g.pz + (yy - g.y0) * g.py + (gx0 + c0 - g.x0));
-      double* dst = sm + L.sring[a] + slot * plane + static_cast<int>(yy - (yb - 2)) * kS3W + c0;
-      mb_expect(&mbar[slot], rbytes);
-      g2s(dst, src, rbytes, &mbar[slot]);
-    }
-  };
-  // Prologue: every plane of the first D + span planes.
-  const int64_t pro_end = min(zb + L.rhi[2] + D, plast + 1);
-  for (int64_t p = zb + L.rlo[2]; p < pro_end; ++p) load_plane(p);
-  __syncthreads();
-  if (tid == 0)
-    for (int64_t p = zb + L.rlo[2]; p < pro_end; ++p) mb_arrive(&mbar[slot_of(p)]);
-  for (int64_t p = zb + L.rlo[2]; p < zb + L.rhi[2]; ++p) mb_wait(&mbar[slot_of(p)], parity_of(p));
-
-  const int64_t px = xb + tx, py = yb + ty;
-  const bool active = px < xe && py < ye;
-  SAcc acc{L, sm, (ty + 2) * kS3W + (tx + 2 + sh), {0, 0, 0, 0, 0}, {}, px, py, zb, red_identity(L.red_op)};
-  int b = 0;  // (z - zb) mod S
-  for (int64_t z = zb; z < zend; ++z) {
-    const int64_t pn = z + L.rhi[2];
-    mb_wait(&mbar[slot_of(pn)], parity_of(pn));  // newest plane this step reads
-    // Refill D planes ahead, into the slot of plane z + rlo_z - 1 (last read
-    // in the previous step, which ended in a barrier).
-    const int64_t pr = pn + D;
-    if (pr <= plast) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      load_plane(pr);
-    }
-    if (active) {
-#pragma unroll
-      for (int k = 0; k < 5; ++k) {  // plane z + k - 2 (k - 2 < rlo_z: never read)
-        const int i = b + k - 2 - L.rlo[2];
-        acc.pofs[k] = (i < 0 ? 0 : i < S ? i : i - S) * plane;
-      }
-      acc.pz = z;
-#pragma unroll
-      for (int a = 0; a < kMaxArgs; ++a) {
-        const UArg& g = L.a[a];
-        acc.g[a] = g.base + ((z - g.z0) * g.pz + (py - g.y0) * g.py + (px - g.x0));
-      }
-      tcb::run_body(BODY, acc, L.prm);
-    }
-    __syncthreads();  // every read of the oldest slot precedes its refill
-    if (pr <= plast && tid == 0) mb_arrive(&mbar[slot_of(pr)]);
-    b = b + 1 == S ? 0 : b + 1;
-  }
-  if (L.has_red) {
-    const double v = block_reduce(acc.acc, L.red_op);
-    if (tid == 0)
-      L.partials[blockIdx.x + static_cast<int64_t>(gridDim.x) * (blockIdx.y + static_cast<int64_t>(gridDim.y) * blockIdx.z)] = v;
-  }
-}
-
-// Periodic ghost fill along dimension D: for every field, the ghost layers
-// [L-depth, L) and [H, H+depth) in dim D take the values at +-N, over the
-// logical box in later dims and the ghost-extended box in earlier dims.
-constexpr int kMaxPeriodic = 16;
-struct PLaunch {
-  int32_t nf, depth;
-  int64_t L[3], H[3];
-  UArg f[kMaxPeriodic];
-};
-
-template <int D>
-__global__ void __launch_bounds__(256) k_periodic(const __grid_constant__ PLaunch P) {
-  // Point grid over (2*depth) x ext(other dims), field index in blockIdx.y.
-  int64_t ext[3], org[3];
-  for (int d = 0; d < 3; ++d) {
-    if (d == D) {
-      ext[d] = 2 * P.depth;
-      org[d] = 0;
-    } else if (d < D) {
-      ext[d] = P.H[d] - P.L[d] + 2 * P.depth;
-      org[d] = P.L[d] - P.depth;
-    } else {
-      ext[d] = P.H[d] - P.L[d];
-      org[d] = P.L[d];
-    }
-  }
-  const int64_t total = ext[0] * ext[1] * ext[2];
-  const UArg& g = P.f[blockIdx.y];
-  const int64_t N = P.H[D] - P.L[D];
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t c[3];
-    c[0] = i % ext[0];
-    c[1] = (i / ext[0]) % ext[1];
-    c[2] = i / (ext[0] * ext[1]);
-    int64_t p[3];
-    for (int d = 0; d < 3; ++d) p[d] = org[d] + c[d];
-    int64_t s[3] = {p[0], p[1], p[2]};
-    if (c[D] < P.depth) {
-      p[D] = P.L[D] - P.depth + c[D];
-      s[D] = p[D] + N;
-    } else {
-      p[D] = P.H[D] + (c[D] - P.depth);
-      s[D] = p[D] - N;
-    }
-    double* dst = g.base + ((p[2] - g.z0) * g.pz + (p[1] - g.y0) * g.py + (p[0] - g.x0));
-    const double* src = g.base + ((s[2] - g.z0) * g.pz + (s[1] - g.y0) * g.py + (s[0] - g.x0));
-    *dst = *src;
-  }
-}
-
-}  // namespace
-
 
 // ---------------------------------------------------------------------------
 // Host side.
@@ -1110,7 +875,7 @@ struct ULaunchRec {
   ULaunch L;
   const void* fn;
   dim3 grid, block;
-  unsigned smem;  // dynamic shared memory (staged 3D walk)
+  unsigned smem;  // dynamic shared memory (none today)
   int64_t nblocks;
   int red;  // >= 0: followed by k_fold into red_dev_[red]
   bool ordered = false;  // Sum folded by k_ordered_sum over the captured contributions
@@ -1188,21 +953,6 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
   static const bool prefetch = [] {
     const char* e = std::getenv("TCG_PREFETCH_L2");
     return !e || std::atoi(e) != 0;
-  }();
-  // Staged 3D walk (k_untiled3s): opt-in with TCG_STAGED3=1. Bit-exact, but
-  // measured 2x slower than the register walk on c3 / 1.5x on c5 (one point
-  // per thread between plane barriers).
-  static const int staged3 = [] {
-    const char* e = std::getenv("TCG_STAGED3");
-    return e ? std::atoi(e) : 0;
-  }();
-  static const int s3_depth = [] {  // planes in flight ahead of the compute
-    const char* e = std::getenv("TCG_S3_D");
-    return e ? std::max(1, std::atoi(e)) : 4;
-  }();
-  static const int s3_zr = [] {
-    const char* e = std::getenv("TCG_S3_ZR");
-    return e ? std::max(1, std::atoi(e)) : 64;
   }();
   const int run_dim = ch.dim == 2 ? ucfg.z : ch.dim == 3 ? ucfg3.z : 4;
 
@@ -1291,37 +1041,6 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
                     static_cast<unsigned>(std::max<int64_t>(1, (n[1] + ucfg3.y - 1) / ucfg3.y)),
                     static_cast<unsigned>(std::max<int64_t>(1, (n[2] + run2 - 1) / run2)));
     }
-    // Staged 3D walk when every read offset is within +-2 and the plane
-    // rings fit in shared memory.
-    bool staged = false;
-    if (ch.dim == 3 && staged3 && L.rmask != 0) {
-      bool reach_ok = true;
-      for (int d = 0; d < 3; ++d) reach_ok = reach_ok && L.rlo[d] >= -2 && L.rhi[d] <= 2;
-      const int nread = __builtin_popcount(static_cast<unsigned>(L.rmask));
-      const int span = L.rhi[2] - L.rlo[2] + 1;
-      for (int ty : {8, 4}) {
-        const int64_t plane = static_cast<int64_t>(ty + 4) * s3::kS3W;
-        // Deepest look-ahead (<= s3_depth planes) whose rings fit.
-        int slots = 0;
-        for (int d = s3_depth; d >= 1 && !slots; --d)
-          if (span + d <= s3::kS3MaxSlots &&
-              static_cast<int64_t>(nread) * (span + d) * plane * 8 <= info_.smem_optin - 1024)
-            slots = span + d;
-        if (!reach_ok || !slots) continue;
-        staged = true;
-        L.sty = ty;
-        L.szr = s3_zr;
-        L.sslots = slots;
-        int k = 0;
-        for (int a = 0; a < lp.nargs; ++a)
-          L.sring[a] = ((L.rmask >> a) & 1) ? static_cast<int32_t>((k++) * slots * plane) : 0;
-        R.smem = static_cast<unsigned>(static_cast<int64_t>(nread) * slots * plane * 8);
-        R.block = dim3(s3::kS3X, static_cast<unsigned>(ty), 1);
-        R.grid = dim3(static_cast<unsigned>((n[0] + s3::kS3X - 1) / s3::kS3X), static_cast<unsigned>((n[1] + ty - 1) / ty),
-                      static_cast<unsigned>((n[2] + s3_zr - 1) / s3_zr));
-        break;
-      }
-    }
     R.nblocks = static_cast<int64_t>(R.grid.x) * R.grid.y * R.grid.z;
     R.red = L.has_red ? lp.red : -1;
     if (L.has_red && red_workers_ > 0 && L.red_op == tcb::kSum && !empty) {
@@ -1343,15 +1062,7 @@ void DeviceExec::run_untiled(const DevChain& ch, double* red_out) {
     // constant inside the kernel.
     const bool known = tcb::dispatch(L.body, [&](auto tag) {
       constexpr int B = decltype(tag)::value;
-      if (staged) {
-        R.fn = reinterpret_cast<const void*>(k_untiled3s<B>);
-        static bool attr_set = false;  // one flag per body instantiation
-        if (!attr_set) {
-          TCG_CK(cudaFuncSetAttribute(k_untiled3s<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(info_.smem_optin) - 1024));
-          attr_set = true;
-        }
-      } else if (ch.dim == 1)
+      if (ch.dim == 1)
         R.fn = reinterpret_cast<const void*>(k_untiled<1, B>);
       else if (ch.dim == 2 && run2 == 2)
         R.fn = reinterpret_cast<const void*>(k_untiled2<B, 2>);

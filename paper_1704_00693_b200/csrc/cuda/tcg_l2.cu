@@ -119,76 +119,6 @@ struct LAcc {
 
 constexpr int kRun = kL2Run;  // rows (2D) / planes (3D) per thread
 
-// Chunk extents per dimension (2D: 32 x 8 threads x kRun rows; 3D: 32 x 8
-// threads x kRun planes; 1D: 256).
-template <int DIM>
-__device__ __forceinline__ int chunk_w(int d) {
-  if (DIM == 1) return 256;
-  if (d == 0) return 32;
-  if (DIM == 2) return 8 * kRun;
-  return d == 1 ? 8 : kRun;
-}
-
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Dataflow wait: every chunk of every conflicting earlier item that lies
-// within `reach` of this chunk must be complete. One warp per dependency.
-template <int DIM>
-__device__ void wait_deps(const L2Launch& P, const DevItem& I, const int c[3]) {
-  const int warp = (threadIdx.x + 32 * threadIdx.y) >> 5, lane = threadIdx.x;
-  int blo[3], bhi[3];
-  for (int d = 0; d < 3; ++d) {
-    if (d < DIM) {
-      blo[d] = I.lo[d] + c[d] * chunk_w<DIM>(d) - P.reach[d];
-      bhi[d] = min(I.hi[d], I.lo[d] + (c[d] + 1) * chunk_w<DIM>(d)) + P.reach[d];
-    } else {
-      blo[d] = 0;
-      bhi[d] = 1;
-    }
-  }
-  for (int q = warp; q < I.ndeps; q += 8) {
-    const DevItem& J = P.items[P.deps[I.dep_off + q]];
-    int c0[3], n[3];
-    bool none = false;
-    for (int d = 0; d < 3; ++d) {
-      if (d >= DIM) {
-        c0[d] = 0;
-        n[d] = 1;
-        continue;
-      }
-      const int lo = max(blo[d], J.lo[d]), hi = min(bhi[d], J.hi[d]);
-      if (lo >= hi) {
-        none = true;
-        break;
-      }
-      c0[d] = (lo - J.lo[d]) / chunk_w<DIM>(d);
-      n[d] = (hi - 1 - J.lo[d]) / chunk_w<DIM>(d) - c0[d] + 1;
-    }
-    if (none) continue;
-    const int jcz = DIM == 3 ? (J.nch / (J.cx * J.cy)) : 1;
-    (void)jcz;
-    for (int k = lane; k < n[0] * n[1] * n[2]; k += 32) {
-      const int kx = k % n[0], r = k / n[0], ky = r % n[1], kz = r / n[1];
-      const int idx = (c0[0] + kx) + J.cx * ((c0[1] + ky) + J.cy * (c0[2] + kz));
-      const uint32_t* f = P.flags + J.flag_off + idx;
-      while (ld_acquire(f) != P.epoch) __nanosleep(64);
-    }
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void signal_chunk(const L2Launch& P, const DevItem& I, uint32_t ch) {
-  __syncthreads();
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    __threadfence();
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + I.flag_off + ch), "r"(P.epoch) : "memory");
-  }
-}
-
 // Points of one item handled by this CTA: chunks of 32 x (8*kRun) (2D),
 // 32 x 8 x kRun (3D) or 256 (1D), grid-strided over the CTAs.
 template <int DIM, int BODY, int LM>
@@ -198,16 +128,11 @@ __device__ __forceinline__ double run_item(const L2Launch& P, const LoopDesc& L,
   const uint32_t nch = static_cast<uint32_t>(I.nch);
   if (DIM == 1) {
     for (uint32_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-      if (P.dataflow) {
-        const int c[3] = {static_cast<int>(ch), 0, 0};
-        wait_deps<DIM>(P, I, c);
-      }
       a.px = I.lo[0] + static_cast<int64_t>(ch) * 256 + threadIdx.x + 32 * threadIdx.y;
       if (a.px < I.hi[0]) {
         a.locate();
         tcb::run_body(BODY, a, prm);
       }
-      if (P.dataflow) signal_chunk(P, I, ch);
     }
     return a.acc;
   }
@@ -215,10 +140,6 @@ __device__ __forceinline__ double run_item(const L2Launch& P, const LoopDesc& L,
   for (uint32_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
     const uint32_t ix = ch % cx, rest = ch / cx;
     const uint32_t iy = DIM == 2 ? rest : rest % cy, iz = DIM == 2 ? 0 : rest / cy;
-    if (P.dataflow) {
-      const int c[3] = {static_cast<int>(ix), static_cast<int>(iy), static_cast<int>(iz)};
-      wait_deps<DIM>(P, I, c);
-    }
     a.px = I.lo[0] + static_cast<int32_t>(ix * 32 + threadIdx.x);
     int r0, rend;
     if (DIM == 2) {
@@ -250,7 +171,6 @@ __device__ __forceinline__ double run_item(const L2Launch& P, const LoopDesc& L,
         }
       }
     }
-    if (P.dataflow) signal_chunk(P, I, ch);
   }
   return a.acc;
 }
@@ -274,7 +194,7 @@ __global__ void __launch_bounds__(256, 4) k_l2tiled(const __grid_constant__ L2La
       v = block_reduce(v, L.red_op);
       if (tid == 0) red_cta[L.red] = red_combine(L.red_op, red_cta[L.red], v);
     }
-    if (I.sync && !P.dataflow) grid.sync();
+    if (I.sync) grid.sync();
   }
   __syncthreads();
   if (tid < P.nred) P.partials[static_cast<int64_t>(tid) * gridDim.x + blockIdx.x] = red_cta[tid];
@@ -356,7 +276,7 @@ void DeviceExec::run_l2(const DevChain& ch, const std::vector<DevItem>& items, c
   P.items = ib->items;
   P.deps = ib->deps;
   P.flags = ib->flags;
-  P.dataflow = deps.empty() ? 0 : 1;
+  P.dataflow = 0;
   P.epoch = ++epoch_;
   for (int d = 0; d < 3; ++d) P.reach[d] = reach[static_cast<size_t>(d)];
   P.params = cd.params;

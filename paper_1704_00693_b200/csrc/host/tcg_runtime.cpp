@@ -826,75 +826,15 @@ void Runtime::run_l2(const LoopChain& chain, const ExecMode& mode, ExecutionRepo
         }
       it = l2_items_.emplace(plan.get(), std::move(li)).first;
     }
-    // Dataflow mode (per-chunk completion flags instead of grid barriers)
-    // is correct but measured slower on the configs (long dependency lists);
-    // opt in with TCG_L2_DATAFLOW=1.
-    static const bool dataflow = [] {
-      const char* e = std::getenv("TCG_L2_DATAFLOW");
-      return e && std::atoi(e) != 0;
-    }();
     DevChain dc = lower(sc, t);
     std::vector<double> out(static_cast<size_t>(std::max(1, dc.nred)));
-    // Item-launch form: every (tile, loop) item of the plan becomes one
-    // untiled-executor launch over the item's range, the whole item list one
-    // CUDA graph (kernel boundaries are the barriers, a tile's data stays in
-    // L2 from item to item). Reducing items get their own partial slots and
-    // are folded here in tile order (executor.cpp:238-240).
-    static const int item_graph = [] {
-      const char* e = std::getenv("TCG_L2_GRAPH");
-      return e ? std::atoi(e) : 0;
-    }();
-    int red_items = 0;
-    for (const DevItem& di : it->second.items) red_items += dc.loops[static_cast<size_t>(di.loop)].red >= 0 ? 1 : 0;
-    if (item_graph && red_items <= 60) {
-      DevChain gi = dc;
-      gi.loops.clear();
-      gi.nred = 0;
-      gi.red_op.clear();
-      std::vector<int> red_of;  // item reduction slot -> sub-chain reduction index
-      for (const DevItem& di : it->second.items) {
-        DevLoop d = dc.loops[static_cast<size_t>(di.loop)];
-        for (int k = 0; k < 3; ++k) {
-          d.range[k][0] = di.lo[k];
-          d.range[k][1] = di.hi[k];
-        }
-        if (d.red >= 0) {
-          red_of.push_back(d.red);
-          gi.red_op.push_back(d.red_op);
-          d.red = gi.nred++;
-        }
-        gi.loops.push_back(d);
-      }
-      std::vector<double> part(static_cast<size_t>(std::max(1, gi.nred)));
-      dev.run_untiled(gi, part.data());
-      for (int r = 0; r < dc.nred; ++r) out[static_cast<size_t>(r)] = red_identity_host(dc.red_op[static_cast<size_t>(r)]);
-      for (int j = 0; j < gi.nred; ++j) {
-        const int r = red_of[static_cast<size_t>(j)];
-        out[static_cast<size_t>(r)] = reduce_combine(static_cast<ReduceOp>(dc.red_op[static_cast<size_t>(r)]),
-                                                     out[static_cast<size_t>(r)], part[static_cast<size_t>(j)]);
-      }
-      for (int i = 0; i < dc.nred; ++i) vals.at(red_base + static_cast<size_t>(i)) = out[static_cast<size_t>(i)];
-      red_base += static_cast<size_t>(dc.nred);
-      last_plan_ = plan;
-      rep.tiles_executed += plan->num_tiles();
-      rep.subchains += 1;
-      rep.ctas += static_cast<int64_t>(it->second.items.size());
-      rep.executor = "tiled-graph";
-      for (int d = 0; d < chain.dim; ++d) {
-        rep.tile_sizes[d] = std::max(rep.tile_sizes[d], std::min<int64_t>(ts[d], int64_t{1} << 30));
-        rep.max_skew[d] = std::max(rep.max_skew[d], plan->max_skew[d]);
-      }
-      continue;
-    }
     static const std::vector<int32_t> no_deps;
-    dev.run_l2(dc, it->second.items, dataflow ? it->second.deps : no_deps, it->second.reach,
-               reinterpret_cast<uint64_t>(plan.get()) ^ (dataflow ? 1 : 0), out.data());
+    dev.run_l2(dc, it->second.items, no_deps, it->second.reach, reinterpret_cast<uint64_t>(plan.get()), out.data());
     for (int i = 0; i < dc.nred; ++i) vals.at(red_base + static_cast<size_t>(i)) = out[static_cast<size_t>(i)];
     red_base += static_cast<size_t>(dc.nred);
     last_plan_ = plan;
     rep.tiles_executed += plan->num_tiles();
-    if (!dataflow)
-      for (const DevItem& di : it->second.items) rep.l2_syncs += di.sync;
+    for (const DevItem& di : it->second.items) rep.l2_syncs += di.sync;
     rep.subchains += 1;
     rep.ctas += static_cast<int64_t>(it->second.items.size());  // items
     for (int d = 0; d < chain.dim; ++d) {

@@ -1,8 +1,8 @@
 """GPU parity of the opt-in executor variants that are selected once per
-process by environment (so each case runs in a child process): the staged
-2.5D 3D walk (TCG_STAGED3=1, shared-memory plane rings filled by bulk
-copies), the item-graph form of the L2-tiled executor (TCG_L2_GRAPH=1), and
-the untiled walk without CUDA graphs / L2 prefetch. Same bar as
+process by environment (so each case runs in a child process): the untiled
+walk without CUDA graphs / L2 prefetch, without the 3D rasterisation bands,
+and the streaming executor's alternative input transports (register loads,
+TMA row copies) and neighbour-only warp synchronisation. Same bar as
 test_gpu_parity.py: fields bit-exact against the oracle, Sum to 1e-12."""
 import os
 import subprocess
@@ -22,7 +22,7 @@ import numpy as np
 import pyoracle
 import chains as C
 from paper_1704_00693_b200 import ExecMode, Runtime, configs
-mode = {{"untiled": ExecMode.untiled(), "tiled": ExecMode.tiled((0, 0, 0))}}[{mode!r}]
+mode = {{"untiled": ExecMode.untiled(), "tiled": ExecMode.tiled((0, 0, 0)), "stream": ExecMode.stream()}}[{mode!r}]
 
 def c3(rt):
     rt.set_default_mode(mode)
@@ -60,11 +60,15 @@ print("ok")
 
 
 @pytest.mark.parametrize("env,mode", [
-    ({"TCG_STAGED3": "1"}, "untiled"),
-    ({"TCG_STAGED3": "1", "TCG_S3_D": "1", "TCG_S3_ZR": "5"}, "untiled"),
     ({"TCG_GRAPHS": "0", "TCG_PREFETCH_L2": "0"}, "untiled"),
-    ({"TCG_L2_GRAPH": "1"}, "tiled"),
-], ids=["staged3", "staged3_shallow", "no_graphs_no_prefetch", "l2_item_graph"])
+    ({"TCG_UNTILED_BAND": "0"}, "untiled"),
+    ({"TCG_UNTILED_BAND": "3"}, "untiled"),
+    ({"TCG_STREAM_INPUT": "0"}, "stream"),
+    ({"TCG_STREAM_INPUT": "1"}, "stream"),
+    ({"TCG_STREAM_NSYNC": "1", "TCG_STREAM_FAST": "1"}, "stream"),
+    ({"TCG_STREAM_OWN_BUDGET": "0", "TCG_STREAM_LOOKAHEAD": "4", "TCG_STREAM_SINGLETON_UNTILED": "0"}, "stream"),
+], ids=["no_graphs_no_prefetch", "no_bands", "bands3", "stream_reg_loads", "stream_tma", "stream_nsync_fast",
+        "stream_own0_la4"])
 def test_variant_matches_oracle(env, mode):
     code = CHILD.format(repo=str(REPO), mode=mode)
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
