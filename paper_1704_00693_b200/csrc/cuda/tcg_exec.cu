@@ -416,6 +416,60 @@ __global__ void __launch_bounds__(256, 6) k_untiled2(const __grid_constant__ ULa
   untiled_block<2, BODY, kUntiledRun>(L);
 }
 
+// Periodic ghost fill along dimension D: for every field, the ghost layers
+// [L-depth, L) and [H, H+depth) in dim D take the values at +-N, over the
+// logical box in later dims and the ghost-extended box in earlier dims.
+constexpr int kMaxPeriodic = 16;
+struct PLaunch {
+  int32_t nf, depth;
+  int64_t L[3], H[3];
+  UArg f[kMaxPeriodic];
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) k_periodic(const __grid_constant__ PLaunch P) {
+  // Point grid over (2*depth) x ext(other dims), field index in blockIdx.y.
+  int64_t ext[3], org[3];
+  for (int d = 0; d < 3; ++d) {
+    if (d == D) {
+      ext[d] = 2 * P.depth;
+      org[d] = 0;
+    } else if (d < D) {
+      ext[d] = P.H[d] - P.L[d] + 2 * P.depth;
+      org[d] = P.L[d] - P.depth;
+    } else {
+      ext[d] = P.H[d] - P.L[d];
+      org[d] = P.L[d];
+    }
+  }
+  const int64_t total = ext[0] * ext[1] * ext[2];
+  const UArg& g = P.f[blockIdx.y];
+  const int64_t N = P.H[D] - P.L[D];
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t c[3];
+    c[0] = i % ext[0];
+    c[1] = (i / ext[0]) % ext[1];
+    c[2] = i / (ext[0] * ext[1]);
+    int64_t p[3];
+    for (int d = 0; d < 3; ++d) p[d] = org[d] + c[d];
+    int64_t s[3] = {p[0], p[1], p[2]};
+    if (c[D] < P.depth) {
+      p[D] = P.L[D] - P.depth + c[D];
+      s[D] = p[D] + N;
+    } else {
+      p[D] = P.H[D] + (c[D] - P.depth);
+      s[D] = p[D] - N;
+    }
+    double* dst = g.base + ((p[2] - g.z0) * g.pz + (p[1] - g.y0) * g.py + (p[0] - g.x0));
+    const double* src = g.base + ((s[2] - g.z0) * g.pz + (s[1] - g.y0) * g.py + (s[0] - g.x0));
+    *dst = *src;
+  }
+}
+
+}  // namespace
+
+
 // ---------------------------------------------------------------------------
 // Host side.
 

@@ -804,6 +804,44 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 )PRE";
 }
 
+// CTA partial of every reduction (warp shuffle, warp partials through sm[],
+// fixed order), then the last CTA to finish folds the CTA partials in CTA
+// order. Expects tid, cta, sm (>= 32 doubles), NT and A in scope.
+void emit_red_epilogue(std::ostringstream& o, const std::vector<std::string>& accs, const std::vector<int>& red_ops, int nt) {
+  if (!accs.empty()) {
+    const int nw = nt / 32;
+    o << "  __syncthreads();\n";
+    for (size_t r = 0; r < accs.size(); ++r) {
+      const int op = red_ops[r];
+      o << "  {\n    double v = " << accs[r] << ";\n";
+      o << "    #pragma unroll\n    for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
+        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
+      o << "    if ((tid & 31) == 0) sm[tid >> 5] = v;\n    __syncthreads();\n";
+      o << "    if (tid < 32) {\n      v = tid < " << nw << " ? sm[tid] : tcgj::ident(" << op << ");\n";
+      o << "      #pragma unroll\n      for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
+        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
+      o << "      if (tid == 0) A.part[" << r << " * gridDim.x + cta] = v;\n    }\n    __syncthreads();\n  }\n";
+    }
+    o << "  __shared__ unsigned int last;\n  __threadfence();\n";
+    o << "  if (tid == 0) last = atomicAdd(A.ticket, 1u) == gridDim.x - 1 ? 1u : 0u;\n  __syncthreads();\n";
+    o << "  if (last) {\n    __threadfence();\n    const int n = gridDim.x;\n";
+    for (size_t r = 0; r < accs.size(); ++r) {
+      const int op = red_ops[r];
+      o << "    {\n      const int chunk = (n + NT - 1) / NT;\n      const int a0 = tid * chunk, a1 = a0 + chunk < n ? a0 + chunk : n;\n";
+      o << "      double v = tcgj::ident(" << op << ");\n";
+      o << "      for (int i = a0; i < a1; ++i) v = tcgj::comb(" << op << ", v, __ldcg(A.part + " << r << " * n + i));\n";
+      o << "      #pragma unroll\n      for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
+        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
+      o << "      if ((tid & 31) == 0) sm[tid >> 5] = v;\n      __syncthreads();\n";
+      o << "      if (tid < 32) {\n        v = tid < " << nw << " ? sm[tid] : tcgj::ident(" << op << ");\n";
+      o << "        #pragma unroll\n        for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
+        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
+      o << "        if (tid == 0) A.out[" << r << "] = v;\n      }\n      __syncthreads();\n    }\n";
+    }
+    o << "    if (tid == 0) *A.ticket = 0u;\n  }\n";
+  }
+}
+
 std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, const Shape& S,
                      const std::vector<StreamGeom>& geoms, const Range* red_mask, const std::vector<int32_t>& param_off,
                      int nparams, StreamKernel& K) {
@@ -1362,39 +1400,241 @@ std::string generate(const LoopChain& ch, const Analysis& A, const Sched& Sc, co
   o << adv.str();
   o << "  }\n";
   if (Sc.ncpa) o << "  tcgj::cp_async_wait<0>();\n";  // nothing may land in the reduction scratch
-  if (!accs.empty()) {
-    const int nw = S.nt / 32;
-    o << "  __syncthreads();\n";
-    for (size_t r = 0; r < accs.size(); ++r) {
-      const int op = red_ops[r];
-      o << "  {\n    double v = " << accs[r] << ";\n";
-      o << "    #pragma unroll\n    for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
-        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
-      o << "    if ((tid & 31) == 0) sm[tid >> 5] = v;\n    __syncthreads();\n";
-      o << "    if (tid < 32) {\n      v = tid < " << nw << " ? sm[tid] : tcgj::ident(" << op << ");\n";
-      o << "      #pragma unroll\n      for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
-        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
-      o << "      if (tid == 0) A.part[" << r << " * gridDim.x + cta] = v;\n    }\n    __syncthreads();\n  }\n";
-    }
-    o << "  __shared__ unsigned int last;\n  __threadfence();\n";
-    o << "  if (tid == 0) last = atomicAdd(A.ticket, 1u) == gridDim.x - 1 ? 1u : 0u;\n  __syncthreads();\n";
-    o << "  if (last) {\n    __threadfence();\n    const int n = gridDim.x;\n";
-    for (size_t r = 0; r < accs.size(); ++r) {
-      const int op = red_ops[r];
-      o << "    {\n      const int chunk = (n + NT - 1) / NT;\n      const int a0 = tid * chunk, a1 = a0 + chunk < n ? a0 + chunk : n;\n";
-      o << "      double v = tcgj::ident(" << op << ");\n";
-      o << "      for (int i = a0; i < a1; ++i) v = tcgj::comb(" << op << ", v, __ldcg(A.part + " << r << " * n + i));\n";
-      o << "      #pragma unroll\n      for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
-        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
-      o << "      if ((tid & 31) == 0) sm[tid >> 5] = v;\n      __syncthreads();\n";
-      o << "      if (tid < 32) {\n        v = tid < " << nw << " ? sm[tid] : tcgj::ident(" << op << ");\n";
-      o << "        #pragma unroll\n        for (int q = 16; q > 0; q >>= 1) v = tcgj::comb(" << op
-        << ", v, __shfl_xor_sync(0xffffffffu, v, q));\n";
-      o << "        if (tid == 0) A.out[" << r << "] = v;\n      }\n      __syncthreads();\n    }\n";
-    }
-    o << "    if (tid == 0) *A.ticket = 0u;\n  }\n";
-  }
+  emit_red_epilogue(o, accs, red_ops, S.nt);
   o << "}\n";
+  return o.str();
+}
+
+
+// ---------------------------------------------------------------- horizontal fusion
+// A run of consecutive loops none of which touches what another one writes
+// (each written dataset is accessed only by its writer, at the iteration
+// point) has no skew and no halo: the loops are independent and can run at
+// every point back to back. The generated kernel is an untiled-style walk --
+// one (x, y) column per thread, RUN rows / planes per thread, inputs read
+// straight from HBM through the read-only path -- calling every body of the
+// run at each point, so a field several loops read through the same stencil
+// is fetched once (the compiler shares the loads across the bodies). c5's RHS
+// loops are such a run: mass / momentum x3 / energy read the same nine fields
+// through radius-2 stars.
+size_t horizontal_run(const LoopChain& ch, size_t begin, size_t limit) {
+  // written: datasets some loop of the run writes (always at the iteration
+  // point); wide: datasets some loop reads through a non-identity stencil.
+  // A loop joins when every dataset it shares with the run's writers is
+  // touched at the iteration point only (a thread then sees its own earlier
+  // write in a register), and nothing it writes was read elsewhere.
+  std::set<DatasetId> written, wide;
+  size_t e = begin;
+  for (; e < ch.loops.size() && e < limit; ++e) {
+    const LoopRecord& lp = ch.loops[e];
+    if (lp.range.empty()) break;
+    if (e > begin && !(lp.range == ch.loops[begin].range)) break;
+    bool ok = true;
+    std::set<DatasetId> w, wd;
+    for (const ArgSpec& a : lp.args) {
+      const bool ident = ch.stencil(a.stencil).is_identity();
+      if (mode_writes(a.mode)) {
+        if (!w.insert(a.dataset).second) ok = false;  // one dataset through two arguments
+        if (wide.count(a.dataset)) ok = false;         // an earlier loop reads its neighbours
+      }
+      if (mode_reads(a.mode) && !ident) {
+        if (written.count(a.dataset)) ok = false;      // neighbours another thread may have rewritten
+        wd.insert(a.dataset);
+      }
+    }
+    for (DatasetId d : wd)
+      if (w.count(d)) ok = false;
+    if (!ok) break;
+    written.insert(w.begin(), w.end());
+    wide.insert(wd.begin(), wd.end());
+  }
+  return e;
+}
+
+std::string generate_horizontal(const LoopChain& ch, const std::vector<StreamGeom>& geoms,
+                                const std::vector<int32_t>& param_off, int nparams, StreamKernel& K, int ntx, int nty,
+                                int run, const Range* red_mask) {
+  std::ostringstream o;
+  const int dim = ch.dim, s = dim - 1;
+  const Range& R = ch.loops[0].range;
+  const int nd = static_cast<int>(K.dats.size());
+  std::map<DatasetId, int> slot_of;
+  for (int k = 0; k < nd; ++k) slot_of[K.dats[static_cast<size_t>(k)]] = k;
+  emit_prelude(o);
+  o << "struct TcgArgs { const double* src[" << nd << "]; double* dst[" << nd
+    << "]; double* part; double* out; unsigned int* ticket; long long ns; double p[" << std::max(1, nparams) << "]; };\n";
+  for (size_t li = 0; li < ch.loops.size(); ++li) {
+    const LoopRecord& lp = ch.loops[li];
+    o << "struct Tr" << li << " {\n  static constexpr int nargs = " << lp.args.size() << ";\n  static constexpr bool red = "
+      << (lp.reduction ? "true" : "false") << ";\n";
+    o << "  static __device__ __forceinline__ int mode(int a) { switch (a) {";
+    for (size_t a = 0; a < lp.args.size(); ++a) o << " case " << a << ": return " << static_cast<int>(lp.args[a].mode) << ";";
+    o << " default: return -1; } }\n";
+    o << "  static __device__ __forceinline__ int npts(int a) { switch (a) {";
+    for (size_t a = 0; a < lp.args.size(); ++a)
+      o << " case " << a << ": return " << ch.stencil(lp.args[a].stencil).points().size() << ";";
+    o << " default: return 0; } }\n";
+    o << "  static __device__ __forceinline__ int pt(int a, int j, int d) { switch ((a * 256 + j) * 4 + d) {";
+    for (size_t a = 0; a < lp.args.size(); ++a) {
+      const auto& pts = ch.stencil(lp.args[a].stencil).points();
+      for (size_t j = 0; j < pts.size(); ++j)
+        for (int d = 0; d < 3; ++d)
+          if (pts[j][static_cast<size_t>(d)] != 0)
+            o << " case " << ((a * 256 + j) * 4 + static_cast<size_t>(d)) << ": return " << pts[j][static_cast<size_t>(d)] << ";";
+    }
+    o << " default: return 0; } }\n};\n";
+  }
+  const int64_t nx = R.extent(0), ny = dim == 3 ? R.extent(1) : 1, nz = R.extent(s);
+  const int64_t nxt = (nx + ntx - 1) / ntx, nyt = dim == 3 ? (ny + nty - 1) / nty : 1;
+  // Reducing runs: every CTA ends with a partial + ticket, so a CTA walks
+  // several RUN-plane chunks (at most ~16K CTAs); others keep one chunk.
+  bool reduces = false;
+  for (const LoopRecord& lp : ch.loops) reduces = reduces || lp.reduction.has_value();
+  const int64_t nzc0 = (nz + run - 1) / run;
+  const int64_t chunks = reduces ? std::max<int64_t>(1, (nxt * nyt * nzc0 + env_int("TCG_STREAM_HRED_CTAS", 16384) - 1) /
+                                                            env_int("TCG_STREAM_HRED_CTAS", 16384))
+                                 : 1;
+  const int64_t nzc = (nzc0 + chunks - 1) / chunks;
+  const int nt = ntx * (dim == 3 ? nty : 1);
+  // y-band rasterisation of the (y, z-chunk) block index (3D), as the untiled walk does.
+  const int64_t band = dim == 3 ? std::min<int64_t>(nyt, std::max<int64_t>(1, env_int("TCG_STREAM_HBAND", 16))) : 1;
+  std::vector<std::string> accs;
+  std::vector<int> red_ops;
+  for (const LoopRecord& lp : ch.loops)
+    if (lp.reduction) {
+      accs.push_back("acc" + std::to_string(accs.size()));
+      red_ops.push_back(static_cast<int>(lp.reduction->op));
+    }
+  K.red_op.assign(red_ops.begin(), red_ops.end());
+  o << "#define NT " << nt << "\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ") tcg_stream(const __grid_constant__ TcgArgs A) {\n";
+  if (!accs.empty()) o << "  __shared__ double sm[64];\n";
+  for (size_t r = 0; r < accs.size(); ++r) o << "  double " << accs[r] << " = tcgj::ident(" << red_ops[r] << ");\n";
+  o << "  const int tid = threadIdx.x;\n  const int tx = tid % " << ntx << ", ty = tid / " << ntx << ";\n  (void)ty;\n";
+  o << "  const long long cta = blockIdx.x;\n  const int ix = static_cast<int>(cta % " << nxt << ");\n";
+  o << "  const long long lin = cta / " << nxt << ";\n";
+  if (dim == 3) {
+    o << "  int iy, iz;\n  {\n    const long long full = " << (nyt / band) * band * nzc << "LL;\n";
+    o << "    if (lin < full) { const long long b = lin / " << band * nzc << ", r = lin - b * " << band * nzc
+      << "; iz = static_cast<int>(r / " << band << "); iy = static_cast<int>(b * " << band << " + (r - static_cast<long long>(iz) * "
+      << band << ")); }\n";
+    o << "    else { const long long w = " << (nyt % band) << ", r = lin - full; iz = static_cast<int>(r / w); iy = static_cast<int>("
+      << (nyt / band) * band << " + (r - static_cast<long long>(iz) * w)); }\n  }\n";
+  } else {
+    o << "  const int iy = 0, iz = static_cast<int>(lin);\n  (void)iy;\n";
+  }
+  o << "  const int x = " << R.start(0) << " + ix * " << ntx << " + tx;\n";
+  if (dim == 3) o << "  const int y = " << R.start(1) << " + iy * " << nty << " + ty;\n";
+  o << "  if (x < " << R.end(0) << (dim == 3 ? " && y < " + std::to_string(R.end(1)) : std::string("")) << ") {\n";
+  o << "  for (int c_ = 0; c_ < " << chunks << "; ++c_) {\n";
+  o << "  const int z0 = " << R.start(s) << " + (iz * " << chunks << " + c_) * " << run << ";\n";
+  std::vector<int64_t> pitch(static_cast<size_t>(nd)), ypitch(static_cast<size_t>(nd));
+  for (int k = 0; k < nd; ++k) {
+    const StreamGeom& G = geoms.at(static_cast<size_t>(K.dats[static_cast<size_t>(k)]));
+    pitch[static_cast<size_t>(k)] = dim == 3 ? G.pz : G.py;
+    ypitch[static_cast<size_t>(k)] = dim == 3 ? G.py : 0;
+    o << "  const long long b" << k << " = static_cast<long long>(z0 - " << (dim == 3 ? G.z0 : G.y0) << ") * " << fmt_L(pitch[static_cast<size_t>(k)]);
+    if (dim == 3) o << " + static_cast<long long>(y - " << G.y0 << ") * " << fmt_L(G.py);
+    o << " + (x - " << G.x0 << ");\n";
+    if (K.store[static_cast<size_t>(k)])
+      o << "  double* __restrict__ const d" << k << " = A.dst[" << k << "] + b" << k << ";\n";
+    else
+      o << "  const double* __restrict__ const s" << k << " = A.src[" << k << "] + b" << k << ";\n";
+  }
+  o << "  #pragma unroll\n  for (int k = 0; k < " << run << "; ++k) {\n    const int z = z0 + k;\n    if (z < " << R.end(s) << ") {\n";
+  // Written datasets: the point's current value lives in c<slot> from the
+  // top of the point to its end (later loops of the run read it there);
+  // loaded first unless the dataset's first access is a pure Write.
+  {
+    std::vector<char> have(static_cast<size_t>(nd), 0);
+    for (const LoopRecord& lp : ch.loops)
+      for (size_t a = 0; a < lp.args.size(); ++a) {
+        const int k = slot_of.at(lp.args[a].dataset);
+        if (!K.store[static_cast<size_t>(k)] || have[static_cast<size_t>(k)]) continue;
+        have[static_cast<size_t>(k)] = 1;
+        bool pure_write = lp.args[a].mode == AccessMode::Write;
+        for (size_t b = 0; b < lp.args.size(); ++b)
+          if (lp.args[b].dataset == lp.args[a].dataset && mode_reads(lp.args[b].mode)) pure_write = false;
+        o << "    double c" << k << " = "
+          << (pure_write ? std::string("0.0") : "d" + std::to_string(k) + "[k * " + fmt_L(pitch[static_cast<size_t>(k)]) + "]") << ";\n";
+      }
+  }
+  size_t racc = 0;
+  for (size_t li = 0; li < ch.loops.size(); ++li) {
+    const LoopRecord& lp = ch.loops[li];
+    o << "    { // loop " << li << ": body " << lp.kernel.fn.body << "\n";
+    for (size_t a = 0; a < lp.args.size(); ++a) {
+      if (!mode_writes(lp.args[a].mode)) continue;
+      const int k = slot_of.at(lp.args[a].dataset);
+      o << "      double o" << a << " = " << (lp.args[a].mode == AccessMode::Write ? std::string("0.0") : "c" + std::to_string(k)) << ";\n";
+    }
+    o << "      auto rd = [&](int a_, int dx_, int dy_, int dz_) -> double {\n";
+    for (size_t a = 0; a < lp.args.size(); ++a) {
+      if (!mode_reads(lp.args[a].mode)) continue;
+      if (mode_writes(lp.args[a].mode)) {
+        o << "        if (a_ == " << a << ") return o" << a << ";\n";
+        continue;
+      }
+      const int k = slot_of.at(lp.args[a].dataset);
+      if (K.store[static_cast<size_t>(k)]) {  // written by a loop of the run: identity reads only (horizontal_run)
+        o << "        if (a_ == " << a << ") return c" << k << ";\n";
+        continue;
+      }
+      // dim 2: (dx, dy) with dy along the walk; dim 3: dz along the walk
+      if (dim == 3)
+        o << "        if (a_ == " << a << ") return __ldg(s" << k << " + ((k + dz_) * " << fmt_L(pitch[static_cast<size_t>(k)]) << " + dy_ * "
+          << fmt_L(ypitch[static_cast<size_t>(k)]) << " + dx_));\n";
+      else
+        o << "        if (a_ == " << a << ") return __ldg(s" << k << " + ((k + dy_) * " << fmt_L(pitch[static_cast<size_t>(k)]) << " + dx_));\n";
+    }
+    o << "        return tcgj::nanv();\n      };\n";
+    o << "      auto wr = [&](int a_, double v_, int inc_) {\n";
+    for (size_t a = 0; a < lp.args.size(); ++a)
+      if (mode_writes(lp.args[a].mode)) o << "        if (a_ == " << a << ") o" << a << " = inc_ ? o" << a << " + v_ : v_;\n";
+    o << "      };\n";
+    if (lp.reduction) {
+      const std::string& acc = accs[racc];
+      const int op = red_ops[racc];
+      ++racc;
+      std::string cond = "true";
+      if (red_mask) {
+        cond = "x >= " + std::to_string(red_mask->start(0)) + " && x < " + std::to_string(red_mask->end(0));
+        if (dim == 3) cond += " && y >= " + std::to_string(red_mask->start(1)) + " && y < " + std::to_string(red_mask->end(1));
+        cond += " && z >= " + std::to_string(red_mask->start(s)) + " && z < " + std::to_string(red_mask->end(s));
+      }
+      o << "      auto ct = [&](double v_) { if (" << cond << ") " << acc << " = tcgj::comb(" << op << ", " << acc << ", v_); };\n";
+    } else {
+      o << "      auto ct = [&](double) {};\n";
+    }
+    o << "      tcgj::Acc<Tr" << li << ", decltype(rd), decltype(wr), decltype(ct)> ac{rd, wr, ct, x, "
+      << (dim == 3 ? "y, z" : "z, 0LL") << "};\n";
+    o << "      tcb::body_t<" << lp.kernel.fn.body << ">(ac, A.p + " << param_off[li] << ");\n";
+    for (size_t a = 0; a < lp.args.size(); ++a) {
+      if (!mode_writes(lp.args[a].mode)) continue;
+      const int k = slot_of.at(lp.args[a].dataset);
+      o << "      c" << k << " = o" << a << ";\n";
+    }
+    o << "    }\n";
+  }
+  for (int k = 0; k < nd; ++k)
+    if (K.store[static_cast<size_t>(k)]) o << "    d" << k << "[k * " << fmt_L(pitch[static_cast<size_t>(k)]) << "] = c" << k << ";\n";
+  o << "    }\n  }\n  }\n  }\n";
+  emit_red_epilogue(o, accs, red_ops, nt);
+  o << "}\n";
+  K.nt = nt;
+  K.minb = 1;
+  K.smem_bytes = 0;
+  K.tiles = nxt * nyt * nzc;
+  K.nctas = K.tiles;
+  K.forced_segments = 1;
+  K.stream_extent = 1;
+  K.tile[0] = ntx;
+  K.tile[1] = dim == 3 ? nty : 1;
+  K.owned[0] = ntx;
+  K.owned[1] = dim == 3 ? nty : 1;
+  K.grid[0] = static_cast<int>(nxt);
+  K.grid[1] = static_cast<int>(nyt);
+  K.grid[2] = static_cast<int>(nzc);
   return o.str();
 }
 
@@ -1529,6 +1769,7 @@ StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeo
     return ns;
   };
   size_t begin = 0;
+  const int horiz = env_int(chain.dim == 2 ? "TCG_STREAM_HORIZ2" : "TCG_STREAM_HORIZ3", env_int("TCG_STREAM_HORIZ", 1));
   while (begin < L) {
     // Sub-chain length (rule measured on B200): the longest
     // prefix that fits the register / shared-memory budget while the
@@ -1559,6 +1800,78 @@ StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeo
       best_end = end;
     }
     if (best_end == 0) throw PlanError("stream executor: a single loop does not fit");
+    // Horizontal runs (independent / own-point-dependent loops over one
+    // range, fused point by point). A vertical prefix that ends inside a
+    // later run of three or more loops is cut back to the run's first loop;
+    // the run starting here wins when it covers at least as many loops as
+    // the vertical prefix (c5: [prim] [mass, mom x3, energy] [update, prim];
+    // c2's 13-loop vertical fusion keeps its two short runs inside).
+    const bool horiz_ok = horiz && choice.max_loops == 0 && choice.nt == 0;
+    const size_t hend = horiz_ok ? horizontal_run(chain, begin, begin + 12) : begin;
+    if (horiz_ok)
+      for (size_t e = begin + 1; e < best_end; ++e) {
+        const size_t re = horizontal_run(chain, e, e + 12);
+        if (re >= e + 3 && re > best_end) {
+          best_end = e;
+          break;
+        }
+      }
+    const bool use_horizontal = horiz_ok && hend >= begin + 2 && hend - begin >= best_end - begin;
+    // Horizontal run: independent loops over one range fused point by point.
+    if (use_horizontal) {
+      {
+        const LoopChain sub = slice_chain(chain, begin, hend);
+        StreamKernel K;
+        K.begin = begin;
+        K.end = hend;
+        K.dim = chain.dim;
+        std::map<DatasetId, int> slot;
+        for (const LoopRecord& lp : sub.loops)
+          for (const ArgSpec& a : lp.args)
+            if (!slot.count(a.dataset)) {
+              slot[a.dataset] = static_cast<int>(K.dats.size());
+              K.dats.push_back(a.dataset);
+            }
+        const size_t nd = K.dats.size();
+        K.load.assign(nd, 1);
+        K.store.assign(nd, 0);
+        K.pingpong.assign(nd, 0);
+        K.store_box.assign(nd, Range(chain.dim));
+        for (const LoopRecord& lp : sub.loops)
+          for (const ArgSpec& a : lp.args)
+            if (mode_writes(a.mode)) {
+              K.store[static_cast<size_t>(slot[a.dataset])] = 1;
+              K.store_box[static_cast<size_t>(slot[a.dataset])] = lp.range;
+            }
+        int np = 0;
+        for (const LoopRecord& lp : sub.loops) {
+          K.param_off.push_back(np);
+          np += static_cast<int>(lp.kernel.fn.params.size());
+        }
+        K.nparams = np;
+        for (const LoopRecord& lp : sub.loops) K.recorded_points += lp.range.volume();
+        K.computed_points = K.recorded_points;
+        K.live_loops = static_cast<int>(sub.size());
+        K.hull = sub.loops[0].range;
+        for (size_t li = 0; li < sub.size(); ++li) {
+          K.loop_range.push_back(sub.loops[li].range);
+          K.loop_live.push_back(1);
+          K.loop_need.push_back(std::array<int64_t, 6>{0, 0, 0, 0, 0, 0});
+        }
+        const int ntx = chain.dim == 3 ? env_int("TCG_STREAM_HNTX", 64) : 128;
+        const int nty = chain.dim == 3 ? env_int("TCG_STREAM_HNTY", 2) : 1;
+        // Measured on c5 (profiles/r5/sweeps.md): 64 x 2 threads; 2 planes per thread 190 ms/step,
+        // 1 plane 202, 3 planes 195, 4 planes 210, 8 planes 209 (registers); 32 x 4 threads 188, 64 x 4 247.
+        const int run = env_int("TCG_STREAM_HRUN", 2);
+        K.source = generate_horizontal(sub, geoms, K.param_off, np, K, ntx, nty, run, red_mask);
+        K.tile_points = static_cast<int64_t>(K.nt) * run;
+        K.warm_rows = 0;
+        K.hash = fnv(K.source);
+        plan.kernels.push_back(std::move(K));
+        begin = hend;
+        continue;
+      }
+    }
     const size_t end = best_end;
     const LoopChain sub = slice_chain(chain, begin, end);
     const Analysis A = analyze(sub, nostore_at(begin, end));

@@ -204,3 +204,45 @@ def test_tiled_auto_picks_among_untiled_and_stream(oracle_lib):
     for k in want[0]:
         assert np.array_equal(got[k], want[0][k]), k
     assert mins == want[1]
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_horizontal_runs_with_own_point_dependencies_and_reductions(oracle_lib, dim):
+    # A run of loops over one range in which written datasets are touched at
+    # the iteration point only: fused point by point into one untiled-style
+    # generated kernel (generate_horizontal) -- independent stencil loops, an
+    # own-point read-modify-write of an earlier loop's output, an increment,
+    # and Sum / Min reductions of values the run itself produced.
+    from paper_1704_00693_b200 import AccessMode, ArgSpec, KernelHandle, Range, ReduceOp, kernels
+    R_, W_, RW_, INC_ = AccessMode.Read, AccessMode.Write, AccessMode.ReadWrite, AccessMode.Increment
+    n = (37, 29) if dim == 2 else (21, 13, 11)
+
+    def run(rt, mode):
+        ident = rt.declare_stencil("id", [(0,) * dim])
+        star = rt.declare_stencil("star", [(0,) * dim] + [tuple((s if e == d else 0) for e in range(dim))
+                                                          for d in range(dim) for s in (-1, 1, 2)])
+        dom = Range(dim, sum(([0, e] for e in n), []))
+        f = [rt.declare_field(f"f{i}", dom) for i in range(5)]
+        rng = np.random.default_rng(11)
+        for i in (0, 1):
+            al = rt.alloc_range(f[i])
+            rt.upload(f[i], rng.random(al.shape()))
+        G = lambda i, s: KernelHandle(i, f"g{i}", kernels.GEN_SUM, (s,))
+        rt.par_loop(G(0, 0.11), dom, [ArgSpec(f[0], star, R_), ArgSpec(f[2], ident, W_)])
+        rt.par_loop(G(1, 0.07), dom, [ArgSpec(f[1], star, R_), ArgSpec(f[0], ident, R_), ArgSpec(f[3], ident, W_)])
+        rt.par_loop(G(2, 0.5), dom, [ArgSpec(f[3], ident, R_), ArgSpec(f[2], ident, RW_)])
+        h0 = rt.par_loop(G(3, 0.25), dom, [ArgSpec(f[2], ident, R_), ArgSpec(f[4], ident, INC_)], ReduceOp.Sum)
+        h1 = rt.par_loop(KernelHandle(4, "min", kernels.GEN_SUM, (1.0,)), dom,
+                         [ArgSpec(f[4], ident, R_), ArgSpec(f[3], ident, RW_)], ReduceOp.Min)
+        rt.flush(mode) if mode is not None else rt.flush()
+        rep = parse_report(rt.report_text()) if hasattr(rt, "report_text") else None
+        return [rt.download(x) for x in f], [rt.fetch_reduction(h0), rt.fetch_reduction(h1)], rep
+
+    want_f, want_r, _ = run(oracle_lib.OracleRuntime(dim), None)
+    rt = Runtime(dim)
+    got_f, got_r, rep = run(rt, ExecMode.stream())
+    for a, b in zip(got_f, want_f):
+        assert np.array_equal(a, b)
+    assert abs(got_r[0] - want_r[0]) <= 1e-12 * abs(want_r[0])
+    assert got_r[1] == want_r[1]
+    assert rep["executor"] == "stream" and int(rep["subchains"]) == 1, rep  # one horizontal kernel

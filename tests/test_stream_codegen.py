@@ -77,3 +77,21 @@ def test_plan_stats_are_consistent():
     # overlapped halos and pipeline warm-up recompute a few percent
     assert recorded == 13 * 4096 * 4096
     assert recorded <= computed <= 1.2 * recorded
+
+
+def test_c5_plan_uses_horizontal_runs(monkeypatch):
+    # c5's RK stage: [prim] [mass, momentum x3, energy] [update, prim of the
+    # next stage]; the last stage ends with [update, kinetic-energy Sum]. The
+    # runs are generated as untiled-style kernels (no shared memory); c2's
+    # 13-loop step stays one vertically fused kernel.
+    monkeypatch.setattr(configs.NsC5, "_initial", lambda self, sb: {})
+    rt = _host_only(Runtime(3))
+    configs.NsC5(rt, 64).enqueue_step()
+    ks = _kernels(rt.stream_plan_pending(compile=True))
+    spans = [re.search(r"loops=\[(\d+),(\d+)\)", k).groups() for k in ks]
+    assert spans == [("0", "1"), ("1", "6"), ("6", "8"), ("8", "13"), ("13", "15"), ("15", "20"), ("20", "22")]
+    assert all("smem=0 " in k for k in ks[1:])
+    rt = _host_only(Runtime(2))
+    configs.HydroC2(rt, 4096).enqueue_step()
+    ks = _kernels(rt.stream_plan_pending())
+    assert len(ks) == 1 and "loops=[0,13)" in ks[0]
