@@ -107,7 +107,15 @@ void* jit_function(const std::string& src, uint64_t hash, int smem_bytes) {
   if (it == g_loaded.end()) {
     std::string cubin;
     const std::string dir = cache_dir();
-    const std::string path = dir.empty() ? "" : dir + "/" + hex(hash) + ".cubin";
+    // The cache key covers the generated source AND the body registry headers
+    // it includes (a cubin cached before a body changed must not be reused).
+    static const uint64_t headers_hash = [] {
+      uint64_t h = 1469598103934665603ull;
+      for (const char* t : {kTcbBodiesSrc, kTcbNsSrc})
+        for (const char* c = t; *c; ++c) h = (h ^ static_cast<unsigned char>(*c)) * 1099511628211ull;
+      return h;
+    }();
+    const std::string path = dir.empty() ? "" : dir + "/" + hex(hash ^ (headers_hash * 0x9E3779B97F4A7C15ull)) + ".cubin";
     if (!path.empty()) {
       std::ifstream f(path, std::ios::binary);
       if (f) {

@@ -224,3 +224,56 @@ def test_hundred_reducing_loops_in_one_flush(mode):
         want.append(20.0 * n * (n - 1) / 2)
     rt.flush(mode)
     assert [rt.fetch_reduction(h) for h in handles] == want
+
+
+def test_step_templates_replay_equals_direct_calls(oracle_lib):
+    # Runtime.record_begin / record_end / replay: the C++ host path re-issues
+    # the recorded par_loop calls (new reduction handles, parameters replaced
+    # in call order); results equal issuing every call from Python.
+    def direct(rt, steps):
+        c = configs.HydroC2(rt, 80)
+        mins = [rt.fetch_reduction(c.enqueue_step()) for _ in range(steps)]
+        return c.outputs(), mins
+
+    want_f, want_m = direct(oracle_lib.OracleRuntime(2), 4)
+    rt = Runtime(2)
+    rt.set_default_mode(ExecMode.tiled_auto())
+    c = configs.HydroC2(rt, 80)
+    rt.record_begin()
+    h = c.enqueue_step()
+    tpl = rt.record_end()
+    mins = [rt.fetch_reduction(h)]
+    for _ in range(3):
+        hs = rt.replay(tpl)
+        assert len(hs) == 1 and rt.pending_loops() == 13
+        mins.append(rt.fetch_reduction(hs[0]))
+    got = c.outputs()
+    for k in want_f:
+        assert np.array_equal(got[k], want_f[k]), k
+    assert mins == want_m
+
+    # parameters replaced per replay (c4's alpha / beta), wrong counts refused
+    from paper_1704_00693_b200.runtime import InvalidArgument
+    cr = configs.CgC4(oracle_lib.OracleRuntime(2), 48)
+    cr.start()
+    for _ in range(5):
+        cr.iterate()
+    rt = Runtime(2)
+    cg = configs.CgC4(rt, 48)
+    cg.start()
+    rt.record_begin()
+    h = cg.enqueue_pq()
+    t0 = rt.record_end()
+    alpha = cg.rr / rt.fetch_reduction(h)
+    rt.record_begin()
+    h = cg.enqueue_update(alpha)
+    t1 = rt.record_end()
+    cg.finish_iteration(rt.fetch_reduction(h))
+    with pytest.raises(InvalidArgument):
+        rt.replay(t0, [1.0, 2.0])  # the template holds one scalar
+    rt.flush()
+    for _ in range(4):
+        alpha = cg.rr / rt.fetch_reduction(rt.replay(t0, [cg.beta])[0])
+        cg.finish_iteration(rt.fetch_reduction(rt.replay(t1, [alpha, alpha])[0]))
+    rel = np.abs(np.array(cg.history) - np.array(cr.history)) / np.abs(np.array(cr.history))
+    assert rel.max() <= 1e-10
