@@ -353,6 +353,14 @@ std::vector<ReductionHandle> Runtime::replay(int id, const double* params, size_
   if (recording_) throw InvalidArgument("replay: a recording is in progress");
   std::vector<ReductionHandle> out;
   size_t pi = 0;
+  if (params) {  // checked before anything is enqueued
+    size_t need = 0;
+    for (const RecordedCall& rc : recorded_[static_cast<size_t>(id)])
+      if (!rc.fill) need += rc.kernel.fn.params.size();
+    if (need != nparams)
+      throw InvalidArgument("replay: the template holds " + std::to_string(need) + " scalar parameters, " +
+                            std::to_string(nparams) + " given");
+  }
   // The template is copied call by call: par_loop consumes its arguments.
   for (size_t i = 0; i < recorded_[static_cast<size_t>(id)].size(); ++i) {
     const RecordedCall& rc = recorded_[static_cast<size_t>(id)][i];

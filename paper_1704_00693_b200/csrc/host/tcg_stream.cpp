@@ -631,7 +631,7 @@ Shape size_kernel(const Analysis& A, const LoopChain& ch, const StreamDevice& de
     S.ns = std::max<int64_t>(1, slots / tiles);
     // Whole waves: round the CTA count to a multiple of the resident slots.
     if (tiles * S.ns < slots) S.ns = std::max<int64_t>(1, (slots + tiles - 1) / tiles);
-    const int64_t min_len = std::max<int64_t>(8, 4 * warm);
+    const int64_t min_len = std::max<int64_t>(8, static_cast<int64_t>(env_dbl("TCG_STREAM_MIN_SEG_WARM", 1.0) * static_cast<double>(warm)));
     S.ns = std::max<int64_t>(1, std::min<int64_t>(S.ns, hs / min_len));
   }
   S.ns = std::max<int64_t>(1, std::min<int64_t>(S.ns, hs));
@@ -1951,7 +1951,11 @@ StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeo
     K.tiles = S.nxt * S.nyt;
     K.stream_extent = A.H.extent(A.s);
     K.warm_rows = A.E[A.s][0] + A.E[A.s][1] + sc.lmax;
-    K.min_seg = std::max<int64_t>(8, env_int("TCG_STREAM_MIN_SEG_WARM", 4) * K.warm_rows);
+    // Shortest segment = TCG_STREAM_MIN_SEG_WARM x the pipeline warm-up. It only binds when the tiles
+    // underfill the GPU (c1: 9 tiles on 592 slots). Measured on c1 (profiles/r5/sweeps.md): 4x warm-up
+    // 0.0539 ms/chain (99 + 207 CTAs), 3x 0.0454, 2x 0.0394, 1x 0.0365 (1233 CTAs) -- short segments
+    // recompute more rows but every CTA walks fewer steps; c2 / c4 (slots already full) are unaffected.
+    K.min_seg = std::max<int64_t>(8, static_cast<int64_t>(env_dbl("TCG_STREAM_MIN_SEG_WARM", 1.0) * static_cast<double>(K.warm_rows)));
     K.tile_points = static_cast<int64_t>(S.tx) * S.ty;
     K.live_loops = nloops_live;
     K.forced_segments = choice.segments;

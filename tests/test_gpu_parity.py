@@ -271,7 +271,7 @@ def test_step_templates_replay_equals_direct_calls(oracle_lib):
     cg.finish_iteration(rt.fetch_reduction(h))
     with pytest.raises(InvalidArgument):
         rt.replay(t0, [1.0, 2.0])  # the template holds one scalar
-    rt.flush()
+    assert rt.pending_loops() == 0  # refused before anything was enqueued
     for _ in range(4):
         alpha = cg.rr / rt.fetch_reduction(rt.replay(t0, [cg.beta])[0])
         cg.finish_iteration(rt.fetch_reduction(rt.replay(t1, [alpha, alpha])[0]))
