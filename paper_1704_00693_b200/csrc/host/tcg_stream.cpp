@@ -1507,7 +1507,10 @@ std::string generate_horizontal(const LoopChain& ch, const std::vector<StreamGeo
     }
   K.red_op.assign(red_ops.begin(), red_ops.end());
   o << "#define NT " << nt << "\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ") tcg_stream(const __grid_constant__ TcgArgs A) {\n";
+  const int hminb = env_int("TCG_STREAM_HMINB", 0);  // register cap through the minimum-blocks launch bound (0 = none)
+  o << "extern \"C\" __global__ void __launch_bounds__(" << nt;
+  if (hminb > 0) o << ", " << hminb;
+  o << ") tcg_stream(const __grid_constant__ TcgArgs A) {\n";
   if (!accs.empty()) o << "  __shared__ double sm[64];\n";
   for (size_t r = 0; r < accs.size(); ++r) o << "  double " << accs[r] << " = tcgj::ident(" << red_ops[r] << ");\n";
   o << "  const int tid = threadIdx.x;\n  const int tx = tid % " << ntx << ", ty = tid / " << ntx << ";\n  (void)ty;\n";
