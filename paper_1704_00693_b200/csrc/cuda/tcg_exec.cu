@@ -354,6 +354,7 @@ __device__ __forceinline__ void untiled_block(const ULaunch& L) {
         // register budget. Measured on c2's CFL loop (plain 91.7 us):
         // 2-row chunks 76.3, 4-row 82.6, the whole 8-row run 100 (spills).
         constexpr int kChunk = kUntiledRun < kBatchRows ? kUntiledRun : kBatchRows;
+        static_assert(kUntiledRun % kChunk == 0, "a run is a whole number of read batches");
 #pragma unroll
         for (int c0 = 0; c0 < kUntiledRun; c0 += kChunk) {
           double buf[kNR > 0 ? kNR * kChunk : 1];
@@ -363,6 +364,10 @@ __device__ __forceinline__ void untiled_block(const ULaunch& L) {
             PreAcc<kNR> pa{g1, buf + k * kNR, 0};
             tcb::run_body(BODY, pa, L.prm);
             g1.advance<DIM>();
+            if (DIM == 2)  // the checked build reports / bounds-checks against the point's coordinates
+              ++g1.py;
+            else
+              ++g1.pz;
           }
 #pragma unroll
           for (int k = 0; k < kChunk; ++k) {
