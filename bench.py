@@ -434,9 +434,10 @@ def main():
     os.environ.setdefault("TCG_AUTOTUNE_FILE", str(REPO / f".tcg_autotune_{args.config}"))
     if os.environ.get("NCCL_DEBUG", "VERSION") == "VERSION":
         os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
-    world, rank, local, dist = dist_setup(args.gpus)
     if args.impl == "reference":
-        return run_reference_arm(args, world, rank, dist)
+        # CPU arm: rank 0 alone works; no process group, no GPU.
+        return run_reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), None)
+    world, rank, local, dist = dist_setup(args.gpus)
 
     import torch
     import paper_1704_00693_b200 as pkg
