@@ -1058,6 +1058,21 @@ void Runtime::run_stream(const LoopChain& chain, ExecutionReport& rep, const Tar
   }
   const StreamPlan& plan = *it->second;
   last_stream_plan_ = it->second;
+  // Every kernel of the plan is compiled / loaded before the first launch, so
+  // a generated kernel NVRTC rejects is a PlanError with no side effects
+  // (tiled_auto then drops the streaming candidate for this chain).
+  const bool sized_plan = stream_choice_.nt == 0 && stream_choice_.bx == 0 && stream_choice_.max_loops == 0;
+  for (const StreamKernel& K : plan.kernels) {
+    if (K.nctas == 0) continue;
+    if (sized_plan && K.end - K.begin == 1 && plan.kernels.size() > 1) continue;  // may run untiled (below)
+    try {
+      jit_function(K.source, K.hash, K.smem_bytes);
+    } catch (const CudaError& e) {
+      if (std::string(e.what()).find("NVRTC compile") != std::string::npos)
+        throw PlanError(std::string("stream executor: ") + e.what());
+      throw;
+    }
+  }
   size_t nred_total = 0;
   for (const StreamKernel& k : plan.kernels) nred_total += k.red_op.size();
   std::vector<uint64_t> buf;
