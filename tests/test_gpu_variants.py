@@ -67,8 +67,10 @@ print("ok")
     ({"TCG_STREAM_INPUT": "1"}, "stream"),
     ({"TCG_STREAM_NSYNC": "1", "TCG_STREAM_FAST": "1"}, "stream"),
     ({"TCG_STREAM_OWN_BUDGET": "0", "TCG_STREAM_LOOKAHEAD": "4", "TCG_STREAM_SINGLETON_UNTILED": "0"}, "stream"),
+    ({"TCG_STREAM_HORIZ": "0", "TCG_STREAM_MIN_SEG_WARM": "4"}, "stream"),
+    ({"TCG_STREAM_HRUN": "3", "TCG_STREAM_HNTX": "32", "TCG_STREAM_HNTY": "4", "TCG_STREAM_HRED_CTAS": "8"}, "stream"),
 ], ids=["no_graphs_no_prefetch", "no_bands", "bands3", "stream_reg_loads", "stream_tma", "stream_nsync_fast",
-        "stream_own0_la4"])
+        "stream_own0_la4", "stream_vertical_only", "stream_horizontal_shapes"])
 def test_variant_matches_oracle(env, mode):
     code = CHILD.format(repo=str(REPO), mode=mode)
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
