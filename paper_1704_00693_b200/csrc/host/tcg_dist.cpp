@@ -194,6 +194,7 @@ std::string schedule_text(const DistSchedule& s, int dim) {
       os << "\n";
     }
   }
+  for (const auto& [ds, depth] : s.wraps) os << "wrap ds=" << ds << " depth=" << depth << "\n";
   for (const HaloMsg& m : s.msgs) {
     os << "msg src=" << m.src << " dst=" << m.dst << " ds=" << m.ds << " dim=" << m.dim << " dir=" << m.dir
        << " box";

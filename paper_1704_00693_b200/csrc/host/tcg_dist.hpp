@@ -41,6 +41,9 @@ struct RankWork {
 struct DistSchedule {
   std::vector<RankWork> ranks;          // every rank of the layout
   std::vector<HaloMsg> msgs;            // global exchange order (dist.cpp:463-511)
+  // Periodic chains: datasets wrapped before the exchange and their depth
+  // (faster dimensions inside every rank, the split one between the end ranks).
+  std::vector<std::pair<DatasetId, int64_t>> wraps;
   std::array<size_t, kMaxDims + 1> phase{0, 0, 0, 0};  // msgs[phase[d], phase[d+1]) exchange along dim d
   int64_t message_bytes = 0;
 };

@@ -1378,12 +1378,15 @@ std::shared_ptr<const DistSchedule> Runtime::dist_schedule(const LoopChain& chai
 DistSchedule Runtime::schedule_pending() {
   if (!grid_set_) throw InvalidArgument("schedule_pending: no rank grid set");
   LoopChain chain = take_pending();
+  std::vector<std::pair<DatasetId, int64_t>> wraps;
   if (!chain.fills.empty()) {
     if (!periodic_domain_)
       throw InvalidArgument("periodic_fill on a rank grid: call set_periodic_domain(true) before set_rank_grid");
     std::vector<Range> logical;
     for (const FieldRec& f : fields_) logical.push_back(f.logical);
-    chain = apply_periodic(chain, logical).chain;
+    PeriodicPlan pp = apply_periodic(chain, logical);
+    chain = std::move(pp.chain);
+    wraps = std::move(pp.pre_fills);
   }
   if (!dist_) {
     // Host-only use (no device): layout and history without rank fields.
@@ -1393,7 +1396,19 @@ DistSchedule Runtime::schedule_pending() {
   }
   std::vector<int64_t> pads;
   for (const FieldRec& f : fields_) pads.push_back(f.pad);
+  // As execute_distributed does: the wrapped points are written before the
+  // schedule is built, so every rank's halo copies of them count as stale.
+  for (const auto& [ds, g] : wraps) {
+    Point wl{0, 0, 0}, wh{0, 0, 0};
+    for (int d = 0; d < dim_; ++d) {
+      wl[d] = -g;
+      wh[d] = g;
+    }
+    dist_->written[ds].push_back(fields_.at(static_cast<size_t>(ds)).logical.dilated(wl, wh));
+    ++dist_->hist_version;
+  }
   DistSchedule s = build_dist_schedule(chain, dist_->layout, pads, &dist_->written);
+  s.wraps = wraps;
   if (note_writes(dist_->written, chain)) ++dist_->hist_version;
   return s;
 }

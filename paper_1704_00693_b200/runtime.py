@@ -297,7 +297,7 @@ def comm_unique_id() -> bytes:
 
 
 def parse_schedule(text: str, dim: int) -> dict:
-    ranks, msgs = {}, []
+    ranks, msgs, wraps = {}, [], []
     for line in text.splitlines():
         f = line.split()
         if not f:
@@ -308,12 +308,14 @@ def parse_schedule(text: str, dim: int) -> dict:
         elif f[0] == "loop":
             nums = [int(v) for v in f[3:]]
             ranks[int(kv["rank"])]["loops"].append([(nums[2 * d], nums[2 * d + 1]) for d in range(dim)])
+        elif f[0] == "wrap":
+            wraps.append((int(kv["ds"]), int(kv["depth"])))
         elif f[0] == "msg":
             i = f.index("box")
             nums = [int(v) for v in f[i + 1:]]
             msgs.append({"src": int(kv["src"]), "dst": int(kv["dst"]), "ds": int(kv["ds"]), "dim": int(kv["dim"]),
                          "dir": int(kv["dir"]), "box": [(nums[2 * d], nums[2 * d + 1]) for d in range(dim)]})
-    return {"ranks": ranks, "msgs": msgs}
+    return {"ranks": ranks, "msgs": msgs, "wraps": wraps}
 
 
 def parse_report(text: str) -> dict:

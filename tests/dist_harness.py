@@ -48,10 +48,13 @@ class DistOracleRank:
     """Same surface as Runtime / OracleRuntime for the workloads in
     tests/chains.py and paper_1704_00693_b200/configs.py."""
 
-    def __init__(self, dim, grid, rank, world):
+    def __init__(self, dim, grid, rank, world, periodic=False, skew=None):
         self.dim, self.rank, self.world = dim, rank, world
         self.grid = list(grid) + [1] * (3 - len(grid))
-        self.sched = Runtime(dim)          # product: queue + schedule (host only)
+        from paper_1704_00693_b200 import RuntimeConfig
+        self.sched = Runtime(dim, RuntimeConfig(skew_allowance=skew) if skew is not None else RuntimeConfig())
+        if periodic:                       # ghost layers join the decomposed domain (before the grid is set)
+            self.sched.set_periodic_domain(True)
         self.sched.set_rank_grid(self.grid)
         self.ora = pyoracle.OracleRuntime(dim)
         self.pending = []                  # (kernel, range, args, red, handle)
@@ -123,12 +126,72 @@ class DistOracleRank:
     def set_default_mode(self, mode):
         pass
 
+    def periodic_fill(self, datasets, depth, logical=None):
+        """Recorded by the product (a PeriodicMark in its queue): the flush's
+        schedule carries the wraps the rewritten chain needs."""
+        self.sched.periodic_fill(datasets, depth, logical)
+
+    def _wrap(self, ds, g):
+        """Periodic wrap of dataset ds to depth g, as Runtime::periodic_exchange
+        does it: the faster dimensions inside this rank over the slabs it
+        holds, the split (slowest) dimension as whole slabs between the end
+        ranks (a self-exchange when there is one rank)."""
+        s = self.dim - 1
+        l = self.local[ds]
+        la = self.ora.alloc_range(l)
+        lg = self.sched.logical_range(ds)
+        L = [lg.start(d) for d in range(self.dim)]
+        H = [lg.end(d) for d in range(self.dim)]
+        lo = [la.start(d) for d in range(self.dim)]
+        arr = self.ora.download(l)
+        z0, z1 = max(la.start(s), L[s]), min(la.end(s), H[s])
+
+        def sl(d, a, b):
+            idx = []
+            for e in reversed(range(self.dim)):
+                if e == d:
+                    idx.append(slice(a - lo[e], b - lo[e]))
+                elif e == s:
+                    idx.append(slice(z0 - lo[e], z1 - lo[e]))
+                elif e < d:
+                    idx.append(slice(L[e] - g - lo[e], H[e] + g - lo[e]))
+                else:
+                    idx.append(slice(L[e] - lo[e], H[e] - lo[e]))
+            return tuple(idx)
+
+        if z1 > z0:
+            for d in range(s):
+                arr[sl(d, L[d] - g, L[d])] = arr[sl(d, H[d] - g, H[d])]
+                arr[sl(d, H[d], H[d] + g)] = arr[sl(d, L[d], L[d] + g)]
+        first, last = 0, self.world - 1
+
+        def slab(a, b):
+            idx = [slice(None)] * self.dim
+            idx[0] = slice(a - lo[s], b - lo[s])   # numpy axis 0 = slowest dimension
+            return tuple(idx)
+
+        for src, dst, s0, d0 in ((last, first, H[s] - g, L[s] - g), (first, last, L[s], H[s])):
+            if src == dst:
+                if self.rank == src:
+                    arr[slab(d0, d0 + g)] = arr[slab(s0, s0 + g)]
+            elif self.rank == src:
+                dist.send(torch.from_numpy(np.ascontiguousarray(arr[slab(s0, s0 + g)])), dst)
+            elif self.rank == dst:
+                buf = torch.empty(arr[slab(d0, d0 + g)].shape, dtype=torch.float64)
+                dist.recv(buf, src)
+                arr[slab(d0, d0 + g)] = buf.numpy()
+            self.halo_messages += 1
+        self.ora.upload(l, arr)
+
     def flush(self, mode=None):
         if not self.pending:
             return {}
         self._ensure_local()
         s = self.sched.schedule_pending()
         assert s["ranks"][self.rank]["owned"] == "x".join(f"[{a},{b})" for a, b in self.owned[self.rank])
+        # Periodic chains: one wrap of the chain's inputs first.
+        for ds, g in s.get("wraps", []):
+            self._wrap(ds, g)
         # One exchange, in the schedule's global order (blocking send/recv
         # pairs: both ends walk the same list).
         for m in s["msgs"]:
