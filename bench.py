@@ -349,40 +349,6 @@ def cpu_reference(cfg_name, k, warmup, budget_s=120.0, mode_pick=None, ny=None):
                       f"RuntimeConfig.threads={threads}, best of untiled/tiled_auto = {mname}"}, None
 
 
-def verify_small(cfg_name, mode):
-    """--verify: the config at a reduced size, three steps, on the GPU (the
-    bench's mode) and on the CPU oracle; fields over the logical box bit for
-    bit, reductions to 1e-12 (Min exact). Returns "pass ..." or "fail ..."."""
-    sys.path.insert(0, str(REPO / "oracle"))
-    import pyoracle
-    from paper_1704_00693_b200 import Runtime
-    n = {"c1": 128, "c2": 160, "c3": 40, "c4": 128, "c5": 24}[cfg_name]
-    dim = 3 if cfg_name in ("c3", "c5") else 2
-
-    def run(rt):
-        c = make_config(cfg_name, rt, n=n)
-        st = Step(cfg_name, c, rt, host="python")
-        for _ in range(3):
-            st()
-        red = list(getattr(c, "history", []))
-        return c.outputs(), red
-
-    pyoracle.load_oracle()
-    fo, ro = run(pyoracle.OracleRuntime(dim))
-    rg = Runtime(dim)
-    rg.set_default_mode(mode)
-    fg, rgv = run(rg)
-    # c4's fields depend on alpha / beta, quotients of Sum reductions whose fold
-    # order differs from the sequential oracle's (1e-12 relative): compared to
-    # 1e-9 there; everywhere else bit for bit.
-    same = (lambda a, b: np.allclose(a, b, rtol=1e-9, atol=1e-12)) if cfg_name == "c4" else np.array_equal
-    bad = [k for k in fo if not same(fo[k], fg[k])]
-    rel = max([abs(a - b) / max(abs(b), 1e-300) for a, b in zip(rgv, ro)], default=0.0)
-    ok = not bad and rel <= 1e-10
-    return (f"{'pass' if ok else 'fail'} ({cfg_name} at n={n}, 3 steps vs the CPU oracle: mismatched_fields={bad}, "
-            f"reduction_max_rel={rel:.3g})")
-
-
 def run_reference_arm(args, world, rank, dist):
     if rank != 0:
         return 0
@@ -414,9 +380,6 @@ def main():
     ap.add_argument("--no-untiled", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=60.0)
     ap.add_argument("--shard", action="store_true", help="c2: use the sharded (NCCL) path even on one GPU")
-    ap.add_argument("--verify", action="store_true",
-                    help="before timing: run the config at a reduced size on the GPU and on the CPU oracle and compare "
-                         "(the reference CLI's --verify, tilechain_cli.cpp:85-92); exit 3 on mismatch")
     ap.add_argument("--report", action="store_true",
                     help="print the last flush's ExecutionReport to stderr (the reference CLI's --report, "
                          "tilechain_cli.cpp:133-136)")
@@ -471,14 +434,6 @@ def main():
         rt.set_default_mode(m)
         cfg = make_config(args.config, rt)
         return rt, cfg, Step(args.config, cfg, rt, host=args.host)
-
-    verify_note = None
-    if args.verify and rank == 0:
-        verify_note = verify_small(args.config, mode)
-        if not verify_note.startswith("pass"):
-            print(f"verify={verify_note}", file=sys.stderr)
-            return 3
-        print(f"verify={verify_note}", file=sys.stderr)
 
     # ---- device-resident throughput (value) ----------------------------------
     rt, cfg, step = build(mode)
@@ -633,7 +588,7 @@ def main():
                            "speedup_vs_untiled": value / untiled_value if untiled_value else None,
                            "tiled_vs_untiled": tiled_value / untiled_value if tiled_value and untiled_value else None,
                            "plan": plans.get(args.mode), "plans": plans},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "verify": verify_note,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}
         print(json.dumps(line))
     if dist is not None:
