@@ -1,6 +1,7 @@
-run c2 base ""
-run c2 ob0la1 "" TCG_STREAM_OWN_BUDGET=0 TCG_STREAM_LOOKAHEAD=1
-run c2 ob8la1 "" TCG_STREAM_OWN_BUDGET=8 TCG_STREAM_LOOKAHEAD=1
-run c2 ob20la1 "" TCG_STREAM_LOOKAHEAD=1
-run c2 ob28 "" TCG_STREAM_OWN_BUDGET=28
-run c2 ob24 "" TCG_STREAM_OWN_BUDGET=24
+run c1 base ""
+run c1 h20 "0,0,0,0,0,20,0,0"
+run c1 h10 "0,0,0,0,0,10,0,0"
+run c1 h7 "0,0,0,0,0,7,0,0"
+run c1 n96 "96,0,0,0,0,0,0,0"
+run c1 n96h10 "96,0,0,0,0,10,0,0"
+run c1 rmax13 "" TCG_STREAM_RMAX2=1.3
