@@ -1773,6 +1773,7 @@ StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeo
   };
   size_t begin = 0;
   const int horiz = env_int(chain.dim == 2 ? "TCG_STREAM_HORIZ2" : "TCG_STREAM_HORIZ3", env_int("TCG_STREAM_HORIZ", 1));
+  const int hmaxl = std::max(2, env_int("TCG_STREAM_HMAXLOOPS", 12));  // loops per horizontal run
   while (begin < L) {
     // Sub-chain length (rule measured on B200): the longest
     // prefix that fits the register / shared-memory budget while the
@@ -1810,10 +1811,10 @@ StreamPlan build_stream_plan(const LoopChain& chain, const std::vector<StreamGeo
     // the vertical prefix (c5: [prim] [mass, mom x3, energy] [update, prim];
     // c2's 13-loop vertical fusion keeps its two short runs inside).
     const bool horiz_ok = horiz && choice.max_loops == 0 && choice.nt == 0;
-    const size_t hend = horiz_ok ? horizontal_run(chain, begin, begin + 12) : begin;
+    const size_t hend = horiz_ok ? horizontal_run(chain, begin, begin + static_cast<size_t>(hmaxl)) : begin;
     if (horiz_ok)
       for (size_t e = begin + 1; e < best_end; ++e) {
-        const size_t re = horizontal_run(chain, e, e + 12);
+        const size_t re = horizontal_run(chain, e, e + static_cast<size_t>(hmaxl));
         if (re >= e + 3 && re > best_end) {
           best_end = e;
           break;
